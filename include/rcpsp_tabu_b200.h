@@ -1,0 +1,160 @@
+/*
+ * rcpsp_tabu_b200.h -- C ABI of the B200-native parallel tabu search for the
+ * RCPSP (drop-in for the hot path of the reference package rcpsp_tabu).
+ *
+ * The reference's plugin seam is its operator layer `rcpsp_tabu/kernels.py`
+ * (backend picked by RCPSP_TABU_BACKEND, kernels.py:25-55): plain functions
+ * over caller-owned int32 arrays, mutating outputs in place.  Each entry point
+ * below replaces one of those operators (or, for rcpsp_solve, the whole
+ * worker/working-set loop of cooperation.orchestrate) with a CUDA launch for
+ * sm_100a.  Conventions:
+ *   - every pointer is caller-owned DEVICE memory unless stated otherwise;
+ *   - all calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy);
+ *   - return 0 on success, <0 on a host-side error; rcpsp_last_error()
+ *     returns a thread-local message.  Device-side invariant violations are
+ *     written to the caller's `err` word (first error wins, see DevErr in
+ *     csrc/common.cuh) and read back only when the caller syncs;
+ *   - an instance is a packed int32 "blob" built by the host packer
+ *     (paper_1711_04556_b200/device.py:pack_instance) from the reference's
+ *     KernelArrays (instance.py:53-80); batches are blobs concatenated with
+ *     an int64 offset table.
+ * No torch types appear here; the Python host passes tensor data_ptr()s.
+ */
+#ifndef RCPSP_TABU_B200_H
+#define RCPSP_TABU_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCPSP_ABI_VERSION 1
+
+/* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
+ * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
+ * B = workers (CTAs) per instance, F = pool_size, T = tabu_size,
+ * n_max = max activities over the batch. */
+typedef struct RcpspSolveArgs {
+    const int32_t *blob;        /* concatenated instance blobs            */
+    const int64_t *blob_off;    /* [I] word offset of each blob           */
+    int64_t n_inst;             /* I                                      */
+    int64_t n_max;              /* max activities                         */
+    int64_t workers;            /* B                                      */
+    int64_t pool_size;          /* F                                      */
+    int64_t tabu_size;          /* T                                      */
+    int64_t delta;              /* swap distance cap                      */
+    int64_t phi_steps;          /* diversification swaps                  */
+    int64_t phi_max;            /* unimproved reads before diversify      */
+    int64_t total_iters;        /* I_total per instance                   */
+    int64_t block_iters;        /* ceil(I_total / B) (search.py:39-42)    */
+    int64_t epoch_limit;        /* planned-iteration limit of this launch */
+    int64_t grant_cap;          /* 0 = uncapped (cooperation.py:317)      */
+    int64_t collect_trace;      /* 1 = write per-iteration traces         */
+    /* working set (cooperation.py:246-273), per instance */
+    int32_t *ws_lock;           /* [I]                                    */
+    int64_t *ws_hdr;            /* [I*16] see WS_* in kernels.cu          */
+    int32_t *ent_order;         /* [I*F*n_max]                            */
+    int32_t *ent_cmax;          /* [I*F]                                  */
+    uint32_t *ent_tabu;         /* [I*F*T] packed (u<<16)|v, 0 = empty    */
+    int32_t *ent_head;          /* [I*F]                                  */
+    int64_t *ent_ic;            /* [I*F] iterations invested              */
+    int64_t *ent_reads;         /* [I*F] reads without improvement        */
+    int32_t *ws_best_order;     /* [I*n_max]                              */
+    /* workers (search.py:107-132), per instance x worker */
+    uint64_t *w_rng;            /* [I*B*6] PCG64 state words              */
+    int64_t *w_stats;           /* [I*B*16] see WK_* in kernels.cu        */
+    int32_t *w_trace;           /* [I*B*trace_cap] or NULL                */
+    int64_t trace_cap;
+    int32_t *w_chunks;          /* [I*B*chunk_cap] chunk lengths or NULL  */
+    int64_t chunk_cap;
+    /* per-CTA scratch */
+    uint32_t *moves_buf;        /* [grid*nbhd_max]                        */
+    int32_t *cmax_buf;          /* [grid*nbhd_max]                        */
+    int64_t nbhd_max;
+    int32_t *err;               /* device error word                      */
+    /* shape maxima of the launch group (shared-memory sizing) */
+    int64_t h_max, e_max, m_max, rmax_max, words;
+    int64_t group;              /* TIME lanes per schedule: 32, 16 or 8   */
+    int64_t threads;            /* threads per CTA                        */
+} RcpspSolveArgs;
+
+int rcpsp_abi_version(void);
+const char *rcpsp_last_error(void);
+
+/* Device properties used for launch sizing: SM count, opt-in smem/CTA. */
+int rcpsp_device_info(int *sm_count, int *smem_optin, int *cc_major, int *cc_minor);
+
+/* Batch of evaluate_order calls (kernels.py:152-194; evaluator.evaluate
+ * evaluator.py:230-246).  orders: [B*n] precedence-feasible permutations.
+ * reverse != 0 evaluates the time-reversed project (successor lists used as
+ * predecessor lists, evaluator.py:336-344).  cmax: [B]; starts: [B*n] or
+ * NULL.  group: TIME lanes per schedule (32/16/8). */
+int rcpsp_eval_batch(const int32_t *blob, int mode, const int32_t *orders, int batch,
+                     int reverse, int32_t *cmax, int32_t *starts, int group, int32_t *err,
+                     void *stream);
+
+/* filter_moves (kernels.py:218-255) over the reduced neighbourhood with
+ * distance cap `delta` for a batch of orders: out_moves [batch*nbhd_cap]
+ * packed (u<<16)|v in lexicographic order, out_count [batch]. */
+int rcpsp_filter_batch(const int32_t *blob, const int32_t *orders, int batch, int delta,
+                       uint32_t *out_moves, int nbhd_cap, int32_t *out_count, void *stream);
+
+/* run_chunk (kernels.py:316-385) for `batch` independent searches on one
+ * instance; one CTA each.  In/out: orders [batch*n], tabu [batch*T] packed,
+ * heads [batch].  In: per-search budget/adopted/start/best_known [batch],
+ * floor.  Out: best_orders [batch*n], trace [batch*trace_cap] (or NULL),
+ * stats [batch*8] = (iters, evals, improved, local_best, cur, head, forced, 0)
+ * -- the reference's 7-tuple.  Tabu counters are rebuilt from the list
+ * (tabu.py:52-60); list entries must satisfy v-u <= delta. */
+int rcpsp_run_chunk_batch(const int32_t *blob, int mode, int delta, int tabu_size, int batch,
+                          int32_t *orders, uint32_t *tabu, int32_t *heads, const int32_t *budget,
+                          const int32_t *adopted, const int32_t *start_cmax,
+                          const int32_t *best_known, int floor_cmax, int32_t *best_orders,
+                          int32_t *trace, int trace_cap, int64_t *stats, uint32_t *moves_buf,
+                          int32_t *cmax_buf, int nbhd_max, int group, int threads, int32_t *err,
+                          void *stream);
+
+/* initialize_working_set (cooperation.py:332-354) for the instances listed in
+ * inst_ids: level-shuffled orders from the pool PCG64 state (one state per
+ * instance, 6 words each: default_rng(seed)), forward-backward improvement
+ * of even entries (evaluator.py:309-368), evaluation, global best. */
+int rcpsp_pool_init(const RcpspSolveArgs *args, const int32_t *inst_ids, int n_ids, int mode,
+                    const uint64_t *pool_rng, void *stream);
+
+/* The search proper (search.run_worker + cooperation.exchange +
+ * Worker.run_adopted): one persistent CTA per (instance, worker), the working
+ * set in HBM behind a per-instance lock, until the planned iterations reach
+ * args->epoch_limit or the global best hits the critical path. */
+int rcpsp_solve(const RcpspSolveArgs *args, const int32_t *inst_ids, int n_ids, int mode,
+                void *stream);
+
+/* Elite exchange between independent populations (multi-GPU, host passes the
+ * all-gathered elites): for every instance, each received elite order whose
+ * makespan beats the worst pool entry replaces it (tabu list cleared, IC and
+ * reads reset); the global best follows.  elites: [n_src*I*n_max] orders,
+ * elite_cmax [n_src*I]. */
+int rcpsp_merge_elites(const RcpspSolveArgs *args, const int32_t *elites,
+                       const int32_t *elite_cmax, int n_src, void *stream);
+
+/* Export each instance's global best (order, cmax) into [I*n_max] / [I]. */
+int rcpsp_export_elites(const RcpspSolveArgs *args, int32_t *elites, int32_t *elite_cmax,
+                        void *stream);
+
+/* diversify (search.py:77-94) for a batch of orders with per-order PCG64
+ * states (advanced in place). */
+int rcpsp_diversify_batch(const int32_t *blob, int32_t *orders, int batch, int phi_steps,
+                          uint64_t *rng, void *stream);
+
+/* Parity probes of the device RNG and Eq. 8 (assigned_iterations,
+ * cooperation.py:233-243). ops: [k*2] (kind, n) with kind 0 = integers(n),
+ * 1 = permutation(arange(n)); out receives the draws back to back. */
+int rcpsp_rng_probe(uint64_t *state, const int32_t *ops, int k, int32_t *out, void *stream);
+int rcpsp_eq8_probe(const int64_t *quad /*[k*4] cmax, ic, block_iters, best*/, int k,
+                    int64_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RCPSP_TABU_B200_H */

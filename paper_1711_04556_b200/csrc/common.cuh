@@ -1,0 +1,98 @@
+// common.cuh -- shared definitions for the B200 tabu-search kernels.
+//
+// Device instance encoding ("blob"): one contiguous int32 array per instance,
+// produced on the host by paper_1711_04556_b200/device.py:pack_instance from
+// the reference's KernelArrays (instance.py:53-80).  The header is 32 words;
+// the arrays follow at the recorded offsets.  The kernels stage the arrays a
+// CTA needs into shared memory once per launch.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FULL_MASK 0xffffffffu
+
+namespace rt {
+
+enum { MODE_CAPACITY = 0, MODE_TIME = 1 };  // kernels.py:22-23
+
+enum BlobField {
+  B_MAGIC = 0, B_N = 1, B_M = 2, B_H = 3, B_E = 4, B_W = 5, B_LB = 6, B_RMAX = 7, B_CPM = 8,
+  B_LEN = 9, B_NLVL = 10,
+  B_OFF_DUR = 16, B_OFF_DEM = 17, B_OFF_CAP = 18, B_OFF_PPTR = 19, B_OFF_PDAT = 20,
+  B_OFF_SPTR = 21, B_OFF_SDAT = 22, B_OFF_REQ = 23, B_OFF_CAPW = 24, B_OFF_LPTR = 25,
+  B_OFF_LDAT = 26,
+  B_HDR = 32
+};
+constexpr int BLOB_MAGIC = 0x52435053;  // "RCPS"
+
+// error codes written to the device error word (first error wins)
+enum DevErr {
+  DE_OK = 0, DE_BAD_BLOB = 1, DE_NO_WINDOW = 2, DE_SMEM = 3, DE_TABU_BAND = 4, DE_CYCLE = 5,
+  DE_BAD_MOVE = 6
+};
+
+__device__ __forceinline__ void set_err(int* err, int code) {
+  if (err) atomicCAS(err, 0, code);
+}
+
+// Shared-memory view of one instance.  All arrays are int32 / uint32.
+struct SInst {
+  int n, m, H, e, W, rmax, cpm;
+  uint32_t hi;           // high bit of every packed resource lane (TIME fits test)
+  const int* dur;        // [n]
+  const uint32_t* req;   // [n*W] packed per-resource demands (TIME)
+  const int* dem;        // [n*m] row-major demands (CAP)
+  const int* cap;        // [m]
+  const uint32_t* capw;  // [W] packed capacities (TIME "full" slot)
+  const int* pptr;       // [n+1]
+  const int* pdat;       // [e]
+  const int* sptr;       // [n+1]
+  const int* sdat;       // [e]
+};
+
+__host__ __device__ __forceinline__ int inst_smem_words(int n, int m, int e, int W) {
+  return n + n * W + n * m + m + W + 2 * (n + 1) + 2 * e;
+}
+
+// Stage a blob into shared memory (all threads of the CTA call this; the
+// caller must __syncthreads() afterwards).  Returns the number of words used.
+__device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int* smem, SInst& I) {
+  I.n = blob[B_N];
+  I.m = blob[B_M];
+  I.H = blob[B_H];
+  I.e = blob[B_E];
+  I.W = blob[B_W];
+  I.rmax = blob[B_RMAX];
+  I.cpm = blob[B_CPM];
+  I.hi = blob[B_LB] == 8 ? 0x80808080u : 0x80008000u;
+  const int n = I.n, m = I.m, e = I.e, W = I.W;
+  int* p = smem;
+  auto copy = [&](int off, int cnt) -> int* {
+    int* dst = p;
+    const int* src = blob + off;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+    p += cnt;
+    return dst;
+  };
+  I.dur = copy(blob[B_OFF_DUR], n);
+  I.req = reinterpret_cast<const uint32_t*>(copy(blob[B_OFF_REQ], n * W));
+  I.dem = copy(blob[B_OFF_DEM], n * m);
+  I.cap = copy(blob[B_OFF_CAP], m);
+  I.capw = reinterpret_cast<const uint32_t*>(copy(blob[B_OFF_CAPW], W));
+  I.pptr = copy(blob[B_OFF_PPTR], n + 1);
+  I.pdat = copy(blob[B_OFF_PDAT], e);
+  I.sptr = copy(blob[B_OFF_SPTR], n + 1);
+  I.sdat = copy(blob[B_OFF_SDAT], e);
+  return static_cast<int>(p - smem);
+}
+
+__device__ __forceinline__ int align4(int words) { return (words + 3) & ~3; }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace rt

@@ -1,0 +1,848 @@
+// kernels.cu -- sm_100a kernels and the C ABI (include/rcpsp_tabu_b200.h).
+//
+// K1 k_eval_batch   evaluate_order over a batch of orders (kernels.py:152-194)
+// K2 k_run_chunk    run_chunk, one CTA per independent search (kernels.py:316-385)
+// K0 k_pool_*       initialize_working_set + FBI (cooperation.py:332-354,
+//                   evaluator.py:289-368), one warp per pool entry
+// K3 k_solve        persistent search: exchange (cooperation.py:276-329) +
+//                   diversify (search.py:77-94) + run_adopted (search.py:144-173)
+//                   per CTA, the working set in HBM behind a per-instance lock
+// K4 k_merge_elites elite exchange between independent populations (multi-GPU)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/rcpsp_tabu_b200.h"
+#include "common.cuh"
+#include "pcg64.cuh"
+#include "search.cuh"
+#include "sgs.cuh"
+
+using namespace rt;
+
+namespace {
+
+enum WsField {
+  WS_CURSOR = 0, WS_TOTAL = 1, WS_PLANNED = 2, WS_CONSUMED = 3, WS_STOP = 4, WS_BEST = 5,
+  WS_BEST_MODE = 6, WS_FLOOR = 7, WS_POOL_EVALS = 8, WS_T0 = 9, WS_T1 = 10
+};
+enum WkField {
+  WK_ITERS = 0, WK_EVALS = 1, WK_EXCH = 2, WK_DIV = 3, WK_FORCED = 4, WK_CHUNKS = 5,
+  WK_TRACE = 6, WK_T0 = 7, WK_T1 = 8
+};
+
+thread_local std::string g_err;
+
+int fail(const std::string& msg) {
+  g_err = msg;
+  return -1;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+struct Hdr {
+  int n, m, H, e, W, lb, rmax, cpm;
+};
+
+}  // namespace
+
+// =========================================================================
+// K1: batch evaluation
+
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob,
+                                                    const int* __restrict__ orders, int batch,
+                                                    int reverse, int* __restrict__ cmax,
+                                                    int* __restrict__ starts, int* err) {
+  extern __shared__ __align__(16) int smem[];
+  SInst I;
+  const int used = align4(stage_instance(blob, smem, I));
+  __syncthreads();
+  const int n = I.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int* pp = reverse ? I.pptr : I.sptr;  // push graph (see sgs.cuh)
+  const int* pd = reverse ? I.pdat : I.sdat;
+  int* scratch = smem + used;
+  if constexpr (MODE == MODE_TIME) {
+    constexpr int S = 32 / G;
+    const int grp = lane / G, lane_g = lane & (G - 1);
+    const int gwords = (I.H + 1) * W + 2 * n;
+    uint32_t* tau = reinterpret_cast<uint32_t*>(scratch + (warp * S + grp) * gwords);
+    int* es = reinterpret_cast<int*>(tau) + (I.H + 1) * W;
+    int* ord = es + n;
+    const int b = (blockIdx.x * nw + warp) * S + grp;
+    const bool active = b < batch;
+    if (active)
+      for (int p = lane_g; p < n; p += G) ord[p] = orders[static_cast<size_t>(b) * n + p];
+    __syncwarp();
+    if (!__any_sync(FULL_MASK, active)) return;
+    const int cm = sgs_time_group<G, W>(I, tau, es, [&](int p) { return ord[p]; }, pp, pd,
+                                        starts ? starts + static_cast<size_t>(b) * n : nullptr,
+                                        active, err);
+    if (active && lane_g == 0) cmax[b] = cm;
+  } else {
+    const int words = cap_thread_words(n, I.m, I.rmax) + n;
+    int* st = scratch + warp * 32 * words;
+    int* ord = st + cap_thread_words(n, I.m, I.rmax) * 32;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    for (int p = 0; p < n; ++p) ord[p * 32 + lane] = orders[static_cast<size_t>(b) * n + p];
+    cmax[b] = sgs_cap_thread(I, st, [&](int p) { return ord[p * 32 + lane]; }, pp, pd,
+                             starts ? starts + static_cast<size_t>(b) * n : nullptr);
+  }
+}
+
+// =========================================================================
+// K2: stand-alone run_chunk (parity / kernels.run_chunk drop-in)
+
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(512) k_run_chunk(
+    const int* __restrict__ blob, int delta, int T, int* orders, uint32_t* tabu, int* heads,
+    const int* budget, const int* adopted, const int* start_cmax, const int* best_known,
+    int floor_cmax, int* best_orders, int* trace, int trace_cap, long long* stats,
+    uint32_t* moves_buf, int* cmax_buf, int nbhd_max, SmemPlan plan, int* err) {
+  extern __shared__ __align__(16) int smem[];
+  const int b = blockIdx.x;
+  CtaCtx c;
+  cta_setup(c, blob, smem, plan, delta, T, moves_buf + static_cast<size_t>(b) * nbhd_max,
+            cmax_buf + static_cast<size_t>(b) * nbhd_max, err);
+  const int n = c.I.n;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    c.base[p] = orders[static_cast<size_t>(b) * n + p];
+    c.best[p] = c.base[p];
+  }
+  for (int i = threadIdx.x; i < T; i += blockDim.x) c.tabu_list[i] = tabu[static_cast<size_t>(b) * T + i];
+  if (threadIdx.x == 0) c.scal[SC_HEAD] = heads[b] % T;
+  __syncthreads();
+  cta_tabu_rebuild(c);
+  ChunkOut o = run_chunk_cta<MODE, G, W>(c, budget[b], adopted[b], start_cmax[b], best_known[b],
+                                         floor_cmax,
+                                         trace ? trace + static_cast<size_t>(b) * trace_cap : nullptr);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    orders[static_cast<size_t>(b) * n + p] = c.base[p];
+    best_orders[static_cast<size_t>(b) * n + p] = c.best[p];
+  }
+  for (int i = threadIdx.x; i < T; i += blockDim.x) tabu[static_cast<size_t>(b) * T + i] = c.tabu_list[i];
+  if (threadIdx.x == 0) {
+    heads[b] = c.scal[SC_HEAD];
+    long long* s = stats + static_cast<size_t>(b) * 8;
+    s[0] = o.iters; s[1] = o.evals; s[2] = o.improved; s[3] = o.local_best; s[4] = o.cur;
+    s[5] = c.scal[SC_HEAD]; s[6] = o.forced; s[7] = 0;
+  }
+}
+
+// =========================================================================
+// filter / diversify / probes
+
+__global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ blob, const int* orders,
+                                                      int delta, uint32_t* out_moves, int nbhd_cap,
+                                                      int* out_count, SmemPlan plan) {
+  extern __shared__ __align__(16) int smem[];
+  const int b = blockIdx.x;
+  CtaCtx c;
+  cta_setup(c, blob, smem, plan, delta, 1, out_moves + static_cast<size_t>(b) * nbhd_cap, nullptr,
+            nullptr);
+  for (int p = threadIdx.x; p < c.I.n; p += blockDim.x)
+    c.base[p] = orders[static_cast<size_t>(b) * c.I.n + p];
+  __syncthreads();
+  const int k = cta_filter(c);
+  if (threadIdx.x == 0) out_count[b] = k;
+}
+
+__global__ void __launch_bounds__(256) k_diversify(const int* __restrict__ blob, int* orders, int steps,
+                                                   uint64_t* rng_words, SmemPlan plan) {
+  extern __shared__ __align__(16) int smem[];
+  const int b = blockIdx.x;
+  CtaCtx c;
+  cta_setup(c, blob, smem, plan, 1, 1, nullptr, nullptr, nullptr);
+  const int n = c.I.n;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) c.base[p] = orders[static_cast<size_t>(b) * n + p];
+  Pcg64 rng;
+  if (threadIdx.x == 0) rng.load(rng_words + static_cast<size_t>(b) * 6);
+  __syncthreads();
+  cta_diversify(c, c.base, steps, rng);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) orders[static_cast<size_t>(b) * n + p] = c.base[p];
+  if (threadIdx.x == 0) rng.store(rng_words + static_cast<size_t>(b) * 6);
+}
+
+__global__ void k_rng_probe(uint64_t* state, const int* ops, int k, int* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Pcg64 g;
+  g.load(state);
+  int o = 0;
+  for (int i = 0; i < k; ++i) {
+    const int kind = ops[2 * i], n = ops[2 * i + 1];
+    if (kind == 0) {
+      out[o++] = static_cast<int>(g.integers(static_cast<uint32_t>(n)));
+    } else {
+      for (int j = 0; j < n; ++j) out[o + j] = j;
+      g.permute(out + o, n);
+      o += n;
+    }
+  }
+  g.store(state);
+}
+
+// Eq. 8, cooperation.py:233-243 (same double-precision operation order)
+__device__ __forceinline__ long long eq8(long long cmax, long long ic, long long block_iters,
+                                         long long best) {
+  const double quality = 0.8 * exp(-100.0 * (static_cast<double>(cmax) / static_cast<double>(best) - 1.0));
+  const double intact = 0.2 * exp(-4.0 * (static_cast<double>(ic) / static_cast<double>(block_iters)));
+  return static_cast<long long>(floor((static_cast<double>(block_iters) / 5.0) * (quality + intact)));
+}
+
+__global__ void k_eq8_probe(const long long* quad, int k, long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = eq8(quad[4 * i], quad[4 * i + 1], quad[4 * i + 2], quad[4 * i + 3]);
+}
+
+// =========================================================================
+// K0: working-set initialisation
+
+// initial_order(shuffle=True) per pool entry (moves.py:42-57); one thread per
+// instance consumes that instance's pool rng sequentially, as the reference.
+__global__ void k_pool_orders(RcpspSolveArgs A, const int* ids, int n_ids,
+                              const uint64_t* pool_rng) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= n_ids) return;
+  const int iid = ids[slot];
+  const int* blob = A.blob + A.blob_off[iid];
+  const int n = blob[B_N], nl = blob[B_NLVL];
+  const int* lptr = blob + blob[B_OFF_LPTR];
+  const int* ldat = blob + blob[B_OFF_LDAT];
+  Pcg64 g;
+  g.load(pool_rng + static_cast<size_t>(iid) * 6);
+  for (int f = 0; f < A.pool_size; ++f) {
+    int* ord = A.ent_order + (static_cast<size_t>(iid) * A.pool_size + f) * A.n_max;
+    for (int l = 0; l < nl; ++l) {
+      const int a = lptr[l], b = lptr[l + 1];
+      for (int i = a; i < b; ++i) ord[i] = ldat[i];
+      if (b - a > 1) g.permute(ord + a, b - a);
+    }
+  }
+}
+
+// one warp evaluates `ord` (TIME: 32-lane group; CAP: lane 0); starts -> smem
+template <int MODE, int W>
+__device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* ord, bool reverse,
+                                         int* starts, int* err) {
+  const int* pp = reverse ? I.pptr : I.sptr;
+  const int* pd = reverse ? I.pdat : I.sdat;
+  int cm;
+  if constexpr (MODE == MODE_TIME) {
+    cm = sgs_time_group<32, W>(I, reinterpret_cast<uint32_t*>(scr), scr + (I.H + 1) * W,
+                               [&](int p) { return ord[p]; }, pp, pd, starts, true, err);
+  } else {
+    cm = 0;
+    if ((threadIdx.x & 31) == 0)
+      cm = sgs_cap_thread(I, scr, [&](int p) { return ord[p]; }, pp, pd, starts);
+    cm = __shfl_sync(FULL_MASK, cm, 0);
+  }
+  __syncwarp();
+  return cm;
+}
+
+// _priority_topo (evaluator.py:289-306) by one warp: repeatedly emit the
+// ready activity with the smallest (key, id).  deg_ptr gives the in-degree.
+__device__ bool warp_ptopo(int n, const int* nxt_ptr, const int* nxt_dat, const int* deg_ptr,
+                           const int* key, int* out, int* indeg, int* ready) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n; i += 32) {
+    indeg[i] = deg_ptr[i + 1] - deg_ptr[i];
+    ready[i] = indeg[i] == 0;
+  }
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {
+    unsigned long long best = ~0ull;
+    for (int i = lane; i < n; i += 32)
+      if (ready[i]) {
+        const unsigned long long kk =
+            (static_cast<unsigned long long>(static_cast<unsigned>(key[i]) ^ 0x80000000u) << 32) |
+            static_cast<unsigned>(i);
+        best = kk < best ? kk : best;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(FULL_MASK, best, o);
+      best = y < best ? y : best;
+    }
+    if (best == ~0ull) return false;
+    const int sel = static_cast<int>(best & 0xffffffffu);
+    __syncwarp();
+    if (lane == 0) {
+      out[k] = sel;
+      ready[sel] = 0;
+    }
+    for (int e = nxt_ptr[sel] + lane; e < nxt_ptr[sel + 1]; e += 32) {
+      const int j = nxt_dat[e];
+      if (--indeg[j] == 0) ready[j] = 1;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+__host__ __device__ inline int pool_entry_words(int mode, int n, int m, int H, int e, int W,
+                                                int rmax) {
+  const int inst = (inst_smem_words(n, m, e, W) + 3) & ~3;
+  const int arrays = 8 * n;  // ord, s1, s2, key, indeg, ready, border/forder, final
+  const int ev = mode == MODE_TIME ? (H + 1) * W + n : 32 * cap_thread_words(n, m, rmax);
+  return inst + arrays + ev + 8;
+}
+
+// forward_backward_improve (evaluator.py:309-368) for even entries, then the
+// evaluation of every entry (cooperation.py:340-351); one warp per entry.
+template <int MODE, int W>
+__global__ void __launch_bounds__(32) k_pool_entry(RcpspSolveArgs A, const int* ids) {
+  extern __shared__ __align__(16) int smem[];
+  const int slot = blockIdx.x / static_cast<int>(A.pool_size);
+  const int f = blockIdx.x % static_cast<int>(A.pool_size);
+  const int iid = ids[slot];
+  const int lane = threadIdx.x;
+  SInst I;
+  const int used = align4(stage_instance(A.blob + A.blob_off[iid], smem, I));
+  __syncthreads();
+  const int n = I.n;
+  int* ord = smem + used;
+  int* s1 = ord + n;
+  int* s2 = s1 + n;
+  int* key = s2 + n;
+  int* indeg = key + n;
+  int* ready = indeg + n;
+  int* tmp = ready + n;
+  int* fin = tmp + n;
+  int* scr = fin + n;
+  int* gord = A.ent_order + (static_cast<size_t>(iid) * A.pool_size + f) * A.n_max;
+  for (int p = lane; p < n; p += 32) ord[p] = gord[p];
+  __syncwarp();
+  long long evals = 0;
+  if (f % 2 == 0) {
+    int cm = warp_eval<MODE, W>(I, scr, ord, false, s1, A.err);
+    ++evals;
+    for (;;) {
+      for (int i = lane; i < n; i += 32) key[i] = -(s1[i] + I.dur[i]);
+      __syncwarp();
+      if (!warp_ptopo(n, I.pptr, I.pdat, I.sptr, key, tmp, indeg, ready)) set_err(A.err, DE_CYCLE);
+      warp_eval<MODE, W>(I, scr, tmp, true, s2, A.err);
+      ++evals;
+      for (int i = lane; i < n; i += 32) key[i] = -(s2[i] + I.dur[i]);
+      __syncwarp();
+      if (!warp_ptopo(n, I.sptr, I.sdat, I.pptr, key, tmp, indeg, ready)) set_err(A.err, DE_CYCLE);
+      const int ncm = warp_eval<MODE, W>(I, scr, tmp, false, s2, A.err);
+      ++evals;
+      if (ncm < cm) {
+        for (int i = lane; i < n; i += 32) s1[i] = s2[i];
+        cm = ncm;
+        __syncwarp();
+      } else {
+        break;
+      }
+    }
+    for (int i = lane; i < n; i += 32) key[i] = s1[i];
+    __syncwarp();
+    if (!warp_ptopo(n, I.sptr, I.sdat, I.pptr, key, fin, indeg, ready)) set_err(A.err, DE_CYCLE);
+    for (int p = lane; p < n; p += 32) ord[p] = fin[p];
+    __syncwarp();
+  }
+  const int cm = warp_eval<MODE, W>(I, scr, ord, false, s2, A.err);
+  ++evals;
+  for (int p = lane; p < n; p += 32) gord[p] = ord[p];
+  if (lane == 0) {
+    A.ent_cmax[static_cast<size_t>(iid) * A.pool_size + f] = cm;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&A.ws_hdr[static_cast<size_t>(iid) * 16 + WS_POOL_EVALS]),
+              static_cast<unsigned long long>(evals));
+  }
+}
+
+// WorkingSet.__init__ (cooperation.py:249-268)
+__global__ void k_pool_finalize(RcpspSolveArgs A, const int* ids, int n_ids, int mode) {
+  const int slot = blockIdx.x;
+  if (slot >= n_ids) return;
+  const int iid = ids[slot];
+  const int* blob = A.blob + A.blob_off[iid];
+  const int n = blob[B_N];
+  __shared__ int s_best;
+  if (threadIdx.x == 0) {
+    int best = 0;
+    const int* cm = A.ent_cmax + static_cast<size_t>(iid) * A.pool_size;
+    for (int i = 1; i < A.pool_size; ++i)
+      if (cm[i] < cm[best]) best = i;
+    s_best = best;
+    int64_t* H = A.ws_hdr + static_cast<size_t>(iid) * 16;
+    H[WS_CURSOR] = 0;
+    H[WS_TOTAL] = A.total_iters;
+    H[WS_PLANNED] = 0;
+    H[WS_CONSUMED] = 0;
+    H[WS_BEST] = cm[best];
+    H[WS_BEST_MODE] = mode;
+    H[WS_FLOOR] = blob[B_CPM];
+    H[WS_STOP] = cm[best] <= blob[B_CPM] ? 1 : 0;
+    H[WS_T0] = 0x7fffffffffffffffll;
+    H[WS_T1] = 0;
+  }
+  __syncthreads();
+  const int* src = A.ent_order + (static_cast<size_t>(iid) * A.pool_size + s_best) * A.n_max;
+  for (int p = threadIdx.x; p < n; p += blockDim.x)
+    A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] = src[p];
+}
+
+// =========================================================================
+// K3: the persistent search (run_worker loop, search.py:176-194)
+
+__device__ __forceinline__ int64_t ldcg64(const int64_t* p) {
+  return static_cast<int64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(512) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
+                                               SmemPlan plan) {
+  extern __shared__ __align__(16) int smem[];
+  const int B = static_cast<int>(A.workers);
+  const int slot = blockIdx.x / B, wk = blockIdx.x % B;
+  const int iid = ids[slot];
+  const int tid = threadIdx.x;
+  const int F = static_cast<int>(A.pool_size), T = static_cast<int>(A.tabu_size);
+  CtaCtx c;
+  cta_setup(c, A.blob + A.blob_off[iid], smem, plan, static_cast<int>(A.delta), T,
+            A.moves_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max,
+            A.cmax_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max, A.err);
+  const int n = c.I.n;
+  const size_t wid = static_cast<size_t>(iid) * B + wk;
+  int64_t* st = A.w_stats + wid * 16;
+  int64_t* Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
+  int* wtrace = A.collect_trace ? A.w_trace + wid * A.trace_cap : nullptr;
+  int* wchunks = A.collect_trace ? A.w_chunks + wid * A.chunk_cap : nullptr;
+  Pcg64 rng;
+  long long s_iters = 0, s_evals = 0, s_exch = 0, s_div = 0, s_forced = 0;
+  long long chunks = st[WK_CHUNKS], tlen = st[WK_TRACE];
+  if (tid == 0) {
+    rng.load(A.w_rng + wid * 6);
+    const unsigned long long t0 = globaltimer();
+    if (st[WK_T0] == 0) st[WK_T0] = static_cast<long long>(t0);
+    atomicMin(reinterpret_cast<unsigned long long*>(&Hd[WS_T0]), t0);
+  }
+  int entry = -1, improved = 0, local_best = 0;
+  long long granted = 0, used = 0;
+  const int floor_cmax = c.I.cpm;
+  for (;;) {
+    // ---------------- exchange (cooperation.py:276-329), under the lock
+    if (tid == 0) {
+      while (atomicCAS(&A.ws_lock[iid], 0, 1) != 0) __nanosleep(100);
+      __threadfence();
+    }
+    __syncthreads();
+    if (entry >= 0) {
+      const size_t eo = static_cast<size_t>(iid) * F + entry;
+      const long long gbest = ldcg64(&Hd[WS_BEST]);
+      if (improved) {
+        int* dst = A.ent_order + eo * A.n_max;
+        for (int p = tid; p < n; p += blockDim.x) dst[p] = c.best[p];
+        uint32_t* tl = A.ent_tabu + eo * T;
+        for (int i = tid; i < T; i += blockDim.x) tl[i] = c.tabu_list[i];
+        if (local_best < gbest) {
+          int* bo = A.ws_best_order + static_cast<size_t>(iid) * A.n_max;
+          for (int p = tid; p < n; p += blockDim.x) bo[p] = c.best[p];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const long long unused = granted - used;
+        Hd[WS_PLANNED] = ldcg64(&Hd[WS_PLANNED]) - (unused > 0 ? unused : 0);
+        Hd[WS_CONSUMED] = ldcg64(&Hd[WS_CONSUMED]) + used;
+        A.ent_ic[eo] = ldcg64(&A.ent_ic[eo]) + used;
+        if (improved) {
+          A.ent_cmax[eo] = local_best;
+          A.ent_head[eo] = c.scal[SC_HEAD];
+          A.ent_reads[eo] = 0;
+          if (local_best < gbest) {
+            Hd[WS_BEST] = local_best;
+            Hd[WS_BEST_MODE] = MODE;
+          }
+        }
+      }
+      entry = -1;
+      improved = 0;
+    }
+    if (tid == 0) {
+      const long long best = ldcg64(&Hd[WS_BEST]);
+      if (best <= ldcg64(&Hd[WS_FLOOR])) Hd[WS_STOP] = 1;
+      const long long planned = ldcg64(&Hd[WS_PLANNED]);
+      if (ldcg64(&Hd[WS_STOP]) || planned >= A.epoch_limit) {
+        c.scal[SC_NONE] = 1;
+      } else {
+        c.scal[SC_NONE] = 0;
+        const long long cursor = ldcg64(&Hd[WS_CURSOR]);
+        const int index = static_cast<int>(cursor % F);
+        Hd[WS_CURSOR] = cursor + 1;
+        const size_t eo = static_cast<size_t>(iid) * F + index;
+        const long long reads = ldcg64(&A.ent_reads[eo]) + 1;
+        A.ent_reads[eo] = reads;
+        const int ecm = __ldcg(&A.ent_cmax[eo]);
+        long long grant = eq8(ecm, ldcg64(&A.ent_ic[eo]), A.block_iters, best);
+        if (grant < 1) grant = 1;
+        if (A.grant_cap > 0 && grant > A.grant_cap) grant = A.grant_cap;
+        const long long room = A.total_iters - planned;
+        const long long eroom = A.epoch_limit - planned;
+        if (grant > room) grant = room;
+        if (grant > eroom) grant = eroom;
+        Hd[WS_PLANNED] = planned + grant;
+        c.scal[SC_ENTRY] = index;
+        c.scal[SC_GRANT] = static_cast<int>(grant);
+        c.scal[SC_ADOPT] = ecm;
+        c.scal[SC_BESTK] = static_cast<int>(best);
+        c.scal[SC_DIV] = reads > A.phi_max ? 1 : 0;
+        c.scal[SC_HEAD] = __ldcg(&A.ent_head[eo]) % T;
+      }
+    }
+    __syncthreads();
+    if (c.scal[SC_NONE]) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicExch(&A.ws_lock[iid], 0);
+      break;
+    }
+    entry = c.scal[SC_ENTRY];
+    granted = c.scal[SC_GRANT];
+    const int adopted = c.scal[SC_ADOPT];
+    const int best_known = c.scal[SC_BESTK];
+    const bool needs_div = c.scal[SC_DIV] != 0;
+    {
+      const size_t eo = static_cast<size_t>(iid) * F + entry;
+      const int* src = A.ent_order + eo * A.n_max;
+      for (int p = tid; p < n; p += blockDim.x) c.base[p] = __ldcg(&src[p]);
+      const uint32_t* tl = A.ent_tabu + eo * T;
+      for (int i = tid; i < T; i += blockDim.x) c.tabu_list[i] = __ldcg(&tl[i]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(&A.ws_lock[iid], 0);
+    cta_tabu_rebuild(c);
+    // ---------------- run_worker body (search.py:189-194)
+    if (needs_div) {
+      cta_diversify(c, c.base, static_cast<int>(A.phi_steps), rng);
+      ++s_div;
+    }
+    ++s_exch;
+    // ---------------- Worker.run_adopted (search.py:144-173)
+    const int start_cmax = cta_eval_one<MODE, G, W>(c, c.base);
+    ++s_evals;
+    for (int p = tid; p < n; p += blockDim.x) c.best[p] = c.base[p];
+    __syncthreads();
+    ChunkOut o = run_chunk_cta<MODE, G, W>(c, static_cast<int>(granted), adopted, start_cmax,
+                                           best_known, floor_cmax,
+                                           wtrace ? wtrace + tlen : nullptr);
+    used = o.iters;
+    improved = o.improved;
+    local_best = o.local_best;
+    s_iters += o.iters;
+    s_evals += o.evals;
+    s_forced += o.forced;
+    if (wtrace) {
+      if (tid == 0 && chunks < A.chunk_cap) wchunks[chunks] = o.iters;
+      ++chunks;
+      tlen += o.iters;
+    }
+  }
+  if (tid == 0) {
+    st[WK_ITERS] += s_iters;
+    st[WK_EVALS] += s_evals;
+    st[WK_EXCH] += s_exch;
+    st[WK_DIV] += s_div;
+    st[WK_FORCED] += s_forced;
+    st[WK_CHUNKS] = chunks;
+    st[WK_TRACE] = tlen;
+    const unsigned long long t1 = globaltimer();
+    st[WK_T1] = static_cast<long long>(t1);
+    atomicMax(reinterpret_cast<unsigned long long*>(&Hd[WS_T1]), t1);
+    rng.store(A.w_rng + wid * 6);
+  }
+}
+
+// =========================================================================
+// K4: elite exchange between populations (multi-GPU)
+
+__global__ void k_export_elites(RcpspSolveArgs A, int* elites, int* elite_cmax) {
+  const int iid = blockIdx.x;
+  const int n = A.blob[A.blob_off[iid] + B_N];
+  for (int p = threadIdx.x; p < A.n_max; p += blockDim.x)
+    elites[static_cast<size_t>(iid) * A.n_max + p] =
+        p < n ? A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] : 0;
+  if (threadIdx.x == 0) elite_cmax[iid] = static_cast<int>(A.ws_hdr[static_cast<size_t>(iid) * 16 + WS_BEST]);
+}
+
+__global__ void k_merge_elites(RcpspSolveArgs A, const int* elites, const int* elite_cmax, int n_src) {
+  const int iid = blockIdx.x;
+  const int n = A.blob[A.blob_off[iid] + B_N];
+  const int F = static_cast<int>(A.pool_size), T = static_cast<int>(A.tabu_size);
+  int64_t* Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
+  __shared__ int s_slot, s_src;
+  for (int s = 0; s < n_src; ++s) {
+    if (threadIdx.x == 0) {
+      s_slot = -1;
+      const int cm = elite_cmax[static_cast<size_t>(s) * A.n_inst + iid];
+      int worst = 0;
+      const int* ec = A.ent_cmax + static_cast<size_t>(iid) * F;
+      bool dup = false;
+      for (int i = 0; i < F; ++i) {
+        if (ec[i] > ec[worst]) worst = i;
+        if (ec[i] == cm) dup = true;  // keep diversity: one entry per makespan value
+      }
+      if (!dup && cm < ec[worst]) {
+        s_slot = worst;
+        s_src = s;
+        const size_t eo = static_cast<size_t>(iid) * F + worst;
+        A.ent_cmax[eo] = cm;
+        A.ent_head[eo] = 0;
+        A.ent_ic[eo] = 0;
+        A.ent_reads[eo] = 0;
+        if (cm < Hd[WS_BEST]) {
+          Hd[WS_BEST] = cm;
+          s_slot = -(worst + 2);  // also copy into the global best
+        }
+      }
+    }
+    __syncthreads();
+    if (s_slot != -1) {
+      const int slot = s_slot >= 0 ? s_slot : -(s_slot + 2);
+      const size_t eo = static_cast<size_t>(iid) * F + slot;
+      const int* src = elites + (static_cast<size_t>(s_src) * A.n_inst + iid) * A.n_max;
+      for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        A.ent_order[eo * A.n_max + p] = src[p];
+        if (s_slot < -1) A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] = src[p];
+      }
+      for (int i = threadIdx.x; i < T; i += blockDim.x) A.ent_tabu[eo * T + i] = 0;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && Hd[WS_BEST] <= Hd[WS_FLOOR]) Hd[WS_STOP] = 1;
+}
+
+// =========================================================================
+// host side
+
+namespace {
+
+int read_hdr(const int32_t* dblob, Hdr& h) {
+  int w[B_HDR];
+  if (cuda_check(cudaMemcpy(w, dblob, sizeof(w), cudaMemcpyDeviceToHost), "read blob header"))
+    return -1;
+  if (w[B_MAGIC] != BLOB_MAGIC) return fail("bad instance blob (magic)");
+  h.n = w[B_N]; h.m = w[B_M]; h.H = w[B_H]; h.e = w[B_E]; h.W = w[B_W]; h.lb = w[B_LB];
+  h.rmax = w[B_RMAX]; h.cpm = w[B_CPM];
+  return 0;
+}
+
+template <class Kern>
+int set_smem(Kern k, size_t bytes) {
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  if (bytes > static_cast<size_t>(optin))
+    return fail("shared memory plan of " + std::to_string(bytes) + " B exceeds the " +
+                std::to_string(optin) + " B per-CTA limit");
+  return cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes)),
+                    "cudaFuncSetAttribute");
+}
+
+int launch_check(const char* what) { return cuda_check(cudaGetLastError(), what); }
+
+// dispatch helper: calls f.template operator()<MODE,G,W>()
+template <class Fn>
+int dispatch(int mode, int group, int words, Fn&& f) {
+  if (mode == MODE_CAPACITY) return f.template operator()<MODE_CAPACITY, 32, 1>();
+  if (mode != MODE_TIME) return fail("mode must be 0 (CAPACITY) or 1 (TIME)");
+  if (words != 1 && words != 2) return fail("TIME packing needs 1 or 2 words per slot");
+  if (group == 32) return words == 1 ? f.template operator()<MODE_TIME, 32, 1>() : f.template operator()<MODE_TIME, 32, 2>();
+  if (group == 16) return words == 1 ? f.template operator()<MODE_TIME, 16, 1>() : f.template operator()<MODE_TIME, 16, 2>();
+  if (group == 8) return words == 1 ? f.template operator()<MODE_TIME, 8, 1>() : f.template operator()<MODE_TIME, 8, 2>();
+  return fail("group must be 32, 16 or 8");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rcpsp_abi_version(void) { return RCPSP_ABI_VERSION; }
+
+const char* rcpsp_last_error(void) { return g_err.c_str(); }
+
+int rcpsp_device_info(int* sm_count, int* smem_optin, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  if (cuda_check(cudaGetDevice(&dev), "cudaGetDevice")) return -1;
+  cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return 0;
+}
+
+int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int batch, int reverse,
+                     int32_t* cmax, int32_t* starts, int group, int32_t* err, void* stream) {
+  if (batch <= 0) return 0;
+  Hdr h;
+  if (read_hdr(blob, h)) return -1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int threads = 256, nw = threads / 32;
+  const int inst = (inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3;
+  return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
+    size_t words;
+    int blocks;
+    if (MODE == MODE_TIME) {
+      words = inst + static_cast<size_t>(nw) * (32 / G) * ((h.H + 1) * W + 2 * h.n);
+      const int per_block = nw * (32 / G);
+      blocks = (batch + per_block - 1) / per_block;
+    } else {
+      words = inst + static_cast<size_t>(nw) * 32 * (cap_thread_words(h.n, h.m, h.rmax) + h.n);
+      blocks = (batch + threads - 1) / threads;
+    }
+    auto k = k_eval_batch<MODE, G, W>;
+    if (set_smem(k, words * 4)) return -1;
+    k<<<blocks, threads, words * 4, s>>>(blob, orders, batch, reverse, cmax, starts, err);
+    return launch_check("k_eval_batch");
+  });
+}
+
+int rcpsp_filter_batch(const int32_t* blob, const int32_t* orders, int batch, int delta,
+                       uint32_t* out_moves, int nbhd_cap, int32_t* out_count, void* stream) {
+  if (batch <= 0) return 0;
+  Hdr h;
+  if (read_hdr(blob, h)) return -1;
+  const int threads = 256;
+  SmemPlan p = plan_smem(MODE_TIME, 32, h.W, h.n, h.m, 0, h.e, h.rmax, delta, 1, 0);
+  if (set_smem(k_filter_batch, p.total * 4)) return -1;
+  k_filter_batch<<<batch, threads, p.total * 4, static_cast<cudaStream_t>(stream)>>>(
+      blob, orders, delta, out_moves, nbhd_cap, out_count, p);
+  return launch_check("k_filter_batch");
+}
+
+int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_size, int batch,
+                          int32_t* orders, uint32_t* tabu, int32_t* heads, const int32_t* budget,
+                          const int32_t* adopted, const int32_t* start_cmax,
+                          const int32_t* best_known, int floor_cmax, int32_t* best_orders,
+                          int32_t* trace, int trace_cap, int64_t* stats, uint32_t* moves_buf,
+                          int32_t* cmax_buf, int nbhd_max, int group, int threads, int32_t* err,
+                          void* stream) {
+  if (batch <= 0) return 0;
+  if (tabu_size < 1) return fail("tabu_size must be >= 1");
+  Hdr h;
+  if (read_hdr(blob, h)) return -1;
+  if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
+    SmemPlan p = plan_smem(MODE, G, W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads / 32);
+    auto k = k_run_chunk<MODE, G, W>;
+    if (set_smem(k, p.total * 4)) return -1;
+    k<<<batch, threads, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
+                                          adopted, start_cmax, best_known, floor_cmax, best_orders,
+                                          trace, trace_cap, reinterpret_cast<long long*>(stats),
+                                          moves_buf, cmax_buf, nbhd_max, p, err);
+    return launch_check("k_run_chunk");
+  });
+}
+
+int rcpsp_pool_init(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, int mode,
+                    const uint64_t* pool_rng, void* stream) {
+  if (n_ids <= 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RcpspSolveArgs A = *args;
+  k_pool_orders<<<(n_ids + 63) / 64, 64, 0, s>>>(A, inst_ids, n_ids,
+                                                 pool_rng);
+  if (launch_check("k_pool_orders")) return -1;
+  const int words = pool_entry_words(mode, static_cast<int>(A.n_max), static_cast<int>(A.m_max),
+                                     static_cast<int>(A.h_max), static_cast<int>(A.e_max),
+                                     static_cast<int>(A.words), static_cast<int>(A.rmax_max));
+  const int grid = n_ids * static_cast<int>(A.pool_size);
+  int rc;
+  if (mode == MODE_CAPACITY) {
+    auto k = k_pool_entry<MODE_CAPACITY, 1>;
+    if (set_smem(k, words * 4)) return -1;
+    k<<<grid, 32, words * 4, s>>>(A, inst_ids);
+    rc = launch_check("k_pool_entry");
+  } else if (A.words == 1) {
+    auto k = k_pool_entry<MODE_TIME, 1>;
+    if (set_smem(k, words * 4)) return -1;
+    k<<<grid, 32, words * 4, s>>>(A, inst_ids);
+    rc = launch_check("k_pool_entry");
+  } else {
+    auto k = k_pool_entry<MODE_TIME, 2>;
+    if (set_smem(k, words * 4)) return -1;
+    k<<<grid, 32, words * 4, s>>>(A, inst_ids);
+    rc = launch_check("k_pool_entry");
+  }
+  if (rc) return rc;
+  k_pool_finalize<<<n_ids, 128, 0, s>>>(A, inst_ids, n_ids, mode);
+  return launch_check("k_pool_finalize");
+}
+
+int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, int mode,
+                void* stream) {
+  if (n_ids <= 0) return 0;
+  RcpspSolveArgs A = *args;
+  const int threads = static_cast<int>(A.threads);
+  if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
+  if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words),
+                  [&]<int MODE, int G, int W>() -> int {
+    SmemPlan p = plan_smem(MODE, G, W, static_cast<int>(A.n_max), static_cast<int>(A.m_max),
+                           static_cast<int>(A.h_max), static_cast<int>(A.e_max),
+                           static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
+                           static_cast<int>(A.tabu_size), threads / 32);
+    auto k = k_solve<MODE, G, W>;
+    if (set_smem(k, p.total * 4)) return -1;
+    const int grid = n_ids * static_cast<int>(A.workers);
+    k<<<grid, threads, p.total * 4, s>>>(A, inst_ids, p);
+    return launch_check("k_solve");
+  });
+}
+
+int rcpsp_export_elites(const RcpspSolveArgs* args, int32_t* elites, int32_t* elite_cmax,
+                        void* stream) {
+  RcpspSolveArgs A = *args;
+  k_export_elites<<<static_cast<int>(A.n_inst), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      A, elites, elite_cmax);
+  return launch_check("k_export_elites");
+}
+
+int rcpsp_merge_elites(const RcpspSolveArgs* args, const int32_t* elites,
+                       const int32_t* elite_cmax, int n_src, void* stream) {
+  RcpspSolveArgs A = *args;
+  k_merge_elites<<<static_cast<int>(A.n_inst), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      A, elites, elite_cmax, n_src);
+  return launch_check("k_merge_elites");
+}
+
+int rcpsp_diversify_batch(const int32_t* blob, int32_t* orders, int batch, int phi_steps,
+                          uint64_t* rng, void* stream) {
+  if (batch <= 0) return 0;
+  Hdr h;
+  if (read_hdr(blob, h)) return -1;
+  SmemPlan p = plan_smem(MODE_TIME, 32, h.W, h.n, h.m, 0, h.e, h.rmax, 1, 1, 0);
+  if (set_smem(k_diversify, p.total * 4)) return -1;
+  k_diversify<<<batch, 256, p.total * 4, static_cast<cudaStream_t>(stream)>>>(
+      blob, orders, phi_steps, rng, p);
+  return launch_check("k_diversify");
+}
+
+int rcpsp_rng_probe(uint64_t* state, const int32_t* ops, int k, int32_t* out, void* stream) {
+  k_rng_probe<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      state, ops, k, out);
+  return launch_check("k_rng_probe");
+}
+
+int rcpsp_eq8_probe(const int64_t* quad, int k, int64_t* out, void* stream) {
+  if (k <= 0) return 0;
+  k_eq8_probe<<<(k + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const long long*>(quad), k, reinterpret_cast<long long*>(out));
+  return launch_check("k_eq8_probe");
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+// search.cuh -- one CTA runs one tabu search (run_chunk, kernels.py:316-385).
+//
+// Per iteration, all in one CTA, nothing leaves the SM except the compacted
+// move list / makespans (L2-resident per-CTA scratch):
+//   filter   Alg. 1 two-phase filter (kernels.py:218-255) as the equivalent
+//            position test  v < minSuccPos(order[u]) && u > maxPredPos(order[v])
+//            over the flat lexicographic neighbourhood, stable block-wide
+//            compaction (ballot bits + block exclusive scan)
+//   evaluate every surviving swap: TIME -> one G-lane group per schedule,
+//            CAP -> one thread per schedule (sgs.cuh)
+//   select   admissible = not tabu or C < aspiration; argmin over the packed
+//            key (C << 16 | rank) = lexicographic tie break (kernels.py:280-309)
+//   apply    swap + tabu_add on the shared-memory circular list with banded
+//            16-bit counters (kernels.py:263-277)
+#pragma once
+#include "common.cuh"
+#include "pcg64.cuh"
+#include "sgs.cuh"
+
+namespace rt {
+
+enum Scal {
+  SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
+  SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_WORDS = 32
+};
+
+struct CtaCtx {
+  SInst I;
+  int delta, T, nbhd;
+  int* base;       // [n] current order
+  int* pos;        // [n] position of each activity
+  int* msp;        // [n] min successor position
+  int* mpp;        // [n] max predecessor position
+  int* rs;         // [n] row start of the flat neighbourhood (rows 1..n-2)
+  int* best;       // [n] best order of the chunk
+  int* rowc;       // [n] diversify row counts
+  uint32_t* tabu_list;  // [T] packed (u << 16) | v, 0 = empty slot
+  uint32_t* tabu_cnt;   // [(n*(delta+1)+1)/2] two 16-bit counters per word
+  int* red;        // [72] reduction scratch
+  int* scal;       // [SC_WORDS]
+  int* evs;        // evaluation scratch (per warp)
+  int warp_words;  // evaluation scratch words per warp
+  uint32_t* moves_buf;  // global [nbhd] compacted moves
+  int* cmax_buf;        // global [nbhd] makespans
+  int* err;
+};
+
+// ---------------------------------------------------------------- block ops
+
+__device__ __forceinline__ unsigned block_min_u32(unsigned v, int* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = __reduce_min_sync(FULL_MASK, v);
+  if (lane == 0) red[warp] = static_cast<int>(v);
+  __syncthreads();
+  if (warp == 0) {
+    unsigned x = lane < nw ? static_cast<unsigned>(red[lane]) : 0xffffffffu;
+    x = __reduce_min_sync(FULL_MASK, x);
+    if (lane == 0) red[64] = static_cast<int>(x);
+  }
+  __syncthreads();
+  const unsigned r = static_cast<unsigned>(red[64]);
+  __syncthreads();
+  return r;
+}
+
+// exclusive scan of one int per thread; *total receives the block sum
+__device__ __forceinline__ int block_excl_scan(int v, int* red, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int x = lane < nw ? red[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, xi, o);
+      if (lane >= o) xi += y;
+    }
+    red[32 + lane] = xi - x;
+    if (lane == 31) red[64] = xi;
+  }
+  __syncthreads();
+  const int r = red[32 + warp] + incl - v;
+  *total = red[64];
+  __syncthreads();
+  return r;
+}
+
+// -------------------------------------------------------------- tabu (SMEM)
+
+__device__ __forceinline__ int tabu_idx(const CtaCtx& c, int u, int v) {
+  return u * (c.delta + 1) + (v - u);
+}
+__device__ __forceinline__ int tabu_get(const CtaCtx& c, int u, int v) {
+  const int i = tabu_idx(c, u, v);
+  return (c.tabu_cnt[i >> 1] >> ((i & 1) * 16)) & 0xffff;
+}
+__device__ __forceinline__ void tabu_bump(const CtaCtx& c, uint32_t mv, int d) {
+  const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+  const int i = tabu_idx(c, u, v);
+  atomicAdd(&c.tabu_cnt[i >> 1], static_cast<uint32_t>(d) << ((i & 1) * 16));
+}
+
+// tabu.py:52-60 (load: rebuild the counter mirror); all threads call
+__device__ __forceinline__ void cta_tabu_rebuild(const CtaCtx& c) {
+  const int words = (c.I.n * (c.delta + 1) + 1) / 2;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) c.tabu_cnt[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < c.T; i += blockDim.x) {
+    const uint32_t mv = c.tabu_list[i];
+    if (mv != 0) {
+      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+      if (v - u < 0 || v - u > c.delta || u >= c.I.n)
+        set_err(c.err, DE_TABU_BAND);
+      else
+        tabu_bump(c, mv, 1);
+    }
+  }
+  __syncthreads();
+}
+
+// kernels.py:263-277 (single thread)
+__device__ __forceinline__ int tabu_add1(const CtaCtx& c, int head, int u, int v) {
+  const uint32_t old = c.tabu_list[head];
+  if (old != 0) {
+    const int ou = static_cast<int>(old >> 16), ov = static_cast<int>(old & 0xffff);
+    const int i = tabu_idx(c, ou, ov);
+    c.tabu_cnt[i >> 1] -= 1u << ((i & 1) * 16);
+  }
+  const uint32_t mv = (static_cast<uint32_t>(u) << 16) | static_cast<uint32_t>(v);
+  c.tabu_list[head] = mv;
+  const int i = tabu_idx(c, u, v);
+  c.tabu_cnt[i >> 1] += 1u << ((i & 1) * 16);
+  return (head + 1) % c.T;
+}
+
+// ----------------------------------------------------------- neighbourhood
+
+// moves.py:60-72 rows: u = 1..n-3, v = u+1..min(u+delta, n-2)
+__device__ __forceinline__ void cta_init_rows(CtaCtx& c) {
+  const int n = c.I.n;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int u = 1; u <= n - 2; ++u) {
+      c.rs[u] = acc;
+      if (u <= n - 3) acc += min(c.delta, n - 2 - u);
+    }
+    c.rs[0] = 0;
+    c.nbhd = n >= 4 ? acc : 0;
+    c.scal[SC_TOTAL] = c.nbhd;
+  }
+  __syncthreads();
+  c.nbhd = c.scal[SC_TOTAL];
+}
+
+__device__ __forceinline__ void decode_move(const CtaCtx& c, int idx, int& u, int& v) {
+  int lo = 1, hi = c.I.n - 3;  // largest u with rs[u] <= idx
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (c.rs[mid] <= idx) lo = mid; else hi = mid - 1;
+  }
+  u = lo;
+  v = u + 1 + (idx - c.rs[u]);
+}
+
+// positions and precedence bounds of `ord`; all threads call
+__device__ __forceinline__ void cta_bounds(const CtaCtx& c, const int* ord) {
+  const int n = c.I.n;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) c.pos[ord[p]] = p;
+  __syncthreads();
+  for (int a = threadIdx.x; a < n; a += blockDim.x) {
+    int lo = 0x7fffffff, hi = -1;
+    for (int e = c.I.sptr[a]; e < c.I.sptr[a + 1]; ++e) lo = min(lo, c.pos[c.I.sdat[e]]);
+    for (int e = c.I.pptr[a]; e < c.I.pptr[a + 1]; ++e) hi = max(hi, c.pos[c.I.pdat[e]]);
+    c.msp[a] = lo;
+    c.mpp[a] = hi;
+  }
+  __syncthreads();
+}
+
+// kernels.py:218-255 -> compacted lexicographic list in moves_buf; returns n_feas
+__device__ __forceinline__ int cta_filter(CtaCtx& c) {
+  cta_bounds(c, c.base);
+  const int nb = c.nbhd, NT = blockDim.x, n = c.I.n;
+  int K = (nb + NT - 1) / NT;
+  K = K < 1 ? 1 : (K > 32 ? 32 : K);
+  int total = 0;
+  for (int tile = 0; tile < nb; tile += NT * K) {
+    const int first = tile + threadIdx.x * K;
+    uint32_t bits = 0;
+    int u0 = 0, v0 = 0;
+    if (first < nb) {
+      decode_move(c, first, u0, v0);
+      int u = u0, v = v0;
+      for (int j = 0; j < K && first + j < nb; ++j) {
+        if (v < c.msp[c.base[u]] && u > c.mpp[c.base[v]]) bits |= 1u << j;
+        if (++v > min(u + c.delta, n - 2)) {
+          ++u;
+          v = u + 1;
+        }
+      }
+    }
+    int tot;
+    int off = block_excl_scan(__popc(bits), c.red, &tot);
+    if (bits) {
+      int u = u0, v = v0;
+      for (int j = 0; j < K && first + j < nb; ++j) {
+        if (bits & (1u << j))
+          c.moves_buf[total + off++] = (static_cast<uint32_t>(u) << 16) | static_cast<uint32_t>(v);
+        if (++v > min(u + c.delta, n - 2)) {
+          ++u;
+          v = u + 1;
+        }
+      }
+    }
+    total += tot;
+  }
+  __syncthreads();
+  return total;
+}
+
+// ------------------------------------------------------------- evaluation
+
+// every compacted move -> cmax_buf (full SGS of the swapped order)
+template <int MODE, int G, int W>
+__device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int* base = c.base;
+  if constexpr (MODE == MODE_TIME) {
+    constexpr int S = 32 / G;
+    const int grp = lane / G;
+    const int gid = warp * S + grp;
+    const int ngroups = nw * S;
+    const int gwords = (c.I.H + 1) * W + c.I.n;
+    uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs + warp * c.warp_words + grp * gwords);
+    int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
+    for (int b = 0; b < n_feas; b += ngroups) {
+      const int idx = b + gid;
+      const bool active = idx < n_feas;
+      if (!__any_sync(FULL_MASK, active)) break;
+      int u = -1, v = -1, au = 0, av = 0;
+      if (active) {
+        const uint32_t mv = c.moves_buf[idx];
+        u = static_cast<int>(mv >> 16);
+        v = static_cast<int>(mv & 0xffff);
+        au = base[v];
+        av = base[u];
+      }
+      const int cm = sgs_time_group<G, W>(
+          c.I, tau, es, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, c.I.sptr,
+          c.I.sdat, nullptr, active, c.err);
+      if (active && (lane & (G - 1)) == 0) c.cmax_buf[idx] = cm;
+    }
+  } else {
+    int* st = c.evs + warp * c.warp_words;
+    for (int idx = threadIdx.x; idx < n_feas; idx += blockDim.x) {
+      const uint32_t mv = c.moves_buf[idx];
+      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+      const int au = base[v], av = base[u];
+      c.cmax_buf[idx] = sgs_cap_thread(
+          c.I, st, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, c.I.sptr,
+          c.I.sdat, nullptr);
+    }
+  }
+  __syncthreads();
+}
+
+// makespan of one order held in shared memory (evaluate_current, search.py:134)
+template <int MODE, int G, int W>
+__device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    int cm;
+    if constexpr (MODE == MODE_TIME) {
+      uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
+      int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
+      cm = sgs_time_group<G, W>(c.I, tau, es, [&](int p) { return ord[p]; }, c.I.sptr, c.I.sdat,
+                                nullptr, lane < G, c.err);
+    } else {
+      cm = 0;
+      if (lane == 0)
+        cm = sgs_cap_thread(c.I, c.evs, [&](int p) { return ord[p]; }, c.I.sptr, c.I.sdat,
+                            nullptr);
+    }
+    if (lane == 0) c.scal[SC_START] = cm;
+  }
+  __syncthreads();
+  return c.scal[SC_START];
+}
+
+// ---------------------------------------------------------------- the chunk
+
+struct ChunkOut {
+  int iters, improved, local_best, cur, forced;
+  long long evals;
+};
+
+// kernels.py:316-385.  c.base holds the order (mutated in place), the tabu
+// list/counters/head are in shared memory.  trace may be null.
+template <int MODE, int G, int W>
+__device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int start_cmax,
+                                  int best_known_cmax, int floor_cmax, int* trace) {
+  const int tid = threadIdx.x, n = c.I.n;
+  int local_best = start_cmax, cur = start_cmax, iters = 0, forced = 0;
+  long long evals = 0;
+  for (int it = 0; it < budget; ++it) {
+    const int n_feas = cta_filter(c);
+    ++iters;
+    if (n_feas == 0) {
+      if (tid == 0 && trace) trace[iters - 1] = cur;
+      break;
+    }
+    cta_eval_moves<MODE, G, W>(c, n_feas);
+    evals += n_feas;
+    const int asp = best_known_cmax < local_best ? best_known_cmax : local_best;
+    unsigned ka = 0xffffffffu, kl = 0xffffffffu;
+    for (int idx = tid; idx < n_feas; idx += blockDim.x) {
+      const unsigned cm = static_cast<unsigned>(c.cmax_buf[idx]);
+      const unsigned key = (cm << 16) | static_cast<unsigned>(idx);
+      kl = min(kl, key);
+      const uint32_t mv = c.moves_buf[idx];
+      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+      if (tabu_get(c, u, v) == 0 || static_cast<int>(cm) < asp) ka = min(ka, key);
+    }
+    ka = block_min_u32(ka, c.red);
+    kl = block_min_u32(kl, c.red);
+    const bool forced_pick = ka == 0xffffffffu;
+    const unsigned key = forced_pick ? kl : ka;
+    forced += forced_pick ? 1 : 0;
+    const int pick = static_cast<int>(key & 0xffff);
+    cur = static_cast<int>(key >> 16);
+    if (tid == 0) {
+      const uint32_t mv = c.moves_buf[pick];
+      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+      const int t = c.base[u];
+      c.base[u] = c.base[v];
+      c.base[v] = t;
+      c.scal[SC_HEAD] = tabu_add1(c, c.scal[SC_HEAD], u, v);
+      if (trace) trace[iters - 1] = cur;
+    }
+    __syncthreads();
+    if (cur < local_best) {
+      local_best = cur;
+      for (int p = tid; p < n; p += blockDim.x) c.best[p] = c.base[p];
+    }
+    if (local_best < adopted_cmax) break;
+    if (local_best <= floor_cmax) break;
+  }
+  __syncthreads();
+  ChunkOut o;
+  o.iters = iters;
+  o.evals = evals;
+  o.improved = local_best < adopted_cmax ? 1 : 0;
+  o.local_best = local_best;
+  o.cur = cur;
+  o.forced = forced;
+  return o;
+}
+
+// ------------------------------------------------------------- diversify
+
+// search.py:77-94: phi_steps uniform feasible swaps over ALL pairs (delta = N),
+// skipped without an RNG draw when nothing is feasible.  rng is thread 0's.
+__device__ void cta_diversify(CtaCtx& c, int* work, int steps, Pcg64& rng) {
+  const int n = c.I.n;
+  for (int s = 0; s < steps; ++s) {
+    cta_bounds(c, work);
+    for (int u = 1 + threadIdx.x; u <= n - 3; u += blockDim.x) {
+      const int lim = c.msp[work[u]];
+      int cnt = 0;
+      for (int v = u + 1; v <= n - 2 && v < lim; ++v) cnt += (u > c.mpp[work[v]]) ? 1 : 0;
+      c.rowc[u] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int total = 0;
+      for (int u = 1; u <= n - 3; ++u) total += c.rowc[u];
+      if (total > 0) {
+        int k = static_cast<int>(rng.integers(static_cast<uint32_t>(total)));
+        int u = 1;
+        while (k >= c.rowc[u]) {
+          k -= c.rowc[u];
+          ++u;
+        }
+        int v = u + 1;
+        for (;; ++v) {
+          if (u > c.mpp[work[v]]) {
+            if (k == 0) break;
+            --k;
+          }
+        }
+        const int t = work[u];
+        work[u] = work[v];
+        work[v] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ shared-memory plan
+
+struct SmemPlan {
+  int inst, base, pos, msp, mpp, rs, best, rowc, tabu_list, tabu_cnt, red, scal, evs;
+  int warp_words, total;
+};
+
+__host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
+                                               int rmax) {
+  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + n);
+  return 32 * cap_thread_words(n, m, rmax);
+}
+
+__host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,
+                                              int rmax, int delta, int T, int nwarps) {
+  SmemPlan p;
+  auto a4 = [](int x) { return (x + 3) & ~3; };
+  int off = 0;
+  p.inst = off; off += a4(inst_smem_words(n, m, e, W));
+  p.base = off; off += a4(n);
+  p.pos = off; off += a4(n);
+  p.msp = off; off += a4(n);
+  p.mpp = off; off += a4(n);
+  p.rs = off; off += a4(n);
+  p.best = off; off += a4(n);
+  p.rowc = off; off += a4(n);
+  p.tabu_list = off; off += a4(T > 0 ? T : 1);
+  p.tabu_cnt = off; off += a4((n * (delta + 1) + 1) / 2);
+  p.red = off; off += 72;
+  p.scal = off; off += SC_WORDS;
+  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax));
+  p.evs = off; off += p.warp_words * nwarps;
+  p.total = off;
+  return p;
+}
+
+__device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem, const SmemPlan& p,
+                                          int delta, int T, uint32_t* moves_buf, int* cmax_buf,
+                                          int* err) {
+  stage_instance(blob, smem + p.inst, c.I);
+  c.delta = delta;
+  c.T = T;
+  c.base = smem + p.base;
+  c.pos = smem + p.pos;
+  c.msp = smem + p.msp;
+  c.mpp = smem + p.mpp;
+  c.rs = smem + p.rs;
+  c.best = smem + p.best;
+  c.rowc = smem + p.rowc;
+  c.tabu_list = reinterpret_cast<uint32_t*>(smem + p.tabu_list);
+  c.tabu_cnt = reinterpret_cast<uint32_t*>(smem + p.tabu_cnt);
+  c.red = smem + p.red;
+  c.scal = smem + p.scal;
+  c.evs = smem + p.evs;
+  c.warp_words = p.warp_words;
+  c.moves_buf = moves_buf;
+  c.cmax_buf = cmax_buf;
+  c.err = err;
+  __syncthreads();
+  cta_init_rows(c);
+}
+
+}  // namespace rt

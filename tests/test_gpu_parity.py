@@ -1,0 +1,270 @@
+"""GPU parity: the sm_100a kernels against the reference's golden vectors and
+the CPU oracle, bit-exact (integer work -- no tolerance anywhere)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import chain_instance, random_topological_order
+
+pytestmark = pytest.mark.gpu
+
+from paper_1711_04556_b200 import (EvalMode, SearchParams, check_schedule_feasible,  # noqa: E402
+                                   critical_path_length, device, evaluate, initial_order,
+                                   orchestrate, orchestrate_batch, synth)
+from paper_1711_04556_b200.cooperation import initialize_working_set  # noqa: E402
+
+GROUPS = (32, 16, 8)
+
+
+@pytest.mark.parametrize("group", GROUPS)
+def test_eval_golden(golden, ginst, group):
+    by_inst: dict = {}
+    for rec in golden["evaluate"]:
+        by_inst.setdefault(rec["instance"], []).append(rec)
+    for name, recs in by_inst.items():
+        orders = np.array([r["order"] for r in recs], np.int32)
+        for mode in (0, 1):
+            c, s = device.eval_batch(ginst[name], orders, mode, group=group)
+            assert c.tolist() == [r[f"cmax{mode}"] for r in recs], (name, mode)
+            assert s.tolist() == [r[f"starts{mode}"] for r in recs], (name, mode)
+
+
+def test_worked_example(ginst):
+    ex = ginst["example12"]
+    s = evaluate(np.array([0, 1, 2, 3, 4, 6, 5, 7, 9, 10, 8, 11]), ex, 1)
+    assert s.cmax == 22 and s.starts.tolist() == [0, 0, 4, 4, 7, 12, 9, 12, 20, 15, 16, 22]
+    assert check_schedule_feasible(ex, s)[0]
+    gap = ginst["gap"]
+    assert evaluate(np.arange(5), gap, 1).cmax == 10
+    assert evaluate(np.arange(5), gap, 0).cmax == 13
+    d2 = ginst["dummy2"]
+    for mode in (0, 1):
+        sch = evaluate(np.array([0, 1]), d2, mode)
+        assert sch.cmax == 0 and sch.starts.tolist() == [0, 0]
+    roomy = ginst["roomy"]
+    for mode in (0, 1):
+        assert evaluate(initial_order(roomy, False), roomy, mode).cmax == critical_path_length(roomy)
+
+
+@pytest.mark.parametrize("cfg,count", [("j30", 4000), ("j60", 3000), ("j120", 3000),
+                                       ("act300", 600)])
+def test_eval_fuzz_vs_oracle(cfg, count):
+    """>= 10^4 random precedence-feasible orders per config, both modes, every
+    group size, starts included; plus reversed-project evaluation."""
+    insts = synth.benchmark_batch(cfg, 2, first_seed=11)
+    rng = np.random.default_rng(5)
+    for inst in insts:
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(count // 2)])
+        for mode in (0, 1):
+            want_c, want_s = oracle.evaluate_batch(inst, orders, mode)
+            for group in GROUPS if mode == 1 else (32,):
+                got_c, got_s = device.eval_batch(inst, orders, mode, group=group)
+                assert np.array_equal(got_c, want_c), (cfg, mode, group)
+                assert np.array_equal(got_s, want_s), (cfg, mode, group)
+        # reversed project (FBI backward pass): orders topological on the reverse graph
+        rev = orders[:, ::-1].copy()
+        for mode in (0, 1):
+            want_c, want_s = oracle.evaluate_batch(inst, rev, mode, reverse=True)
+            got_c, got_s = device.eval_batch(inst, rev, mode, reverse=True)
+            assert np.array_equal(got_c, want_c) and np.array_equal(got_s, want_s)
+
+
+def test_eval_fuzz_small_shapes():
+    """Varied shapes: 1-8 resources, 8/16-bit lanes, tiny and long durations."""
+    rng = np.random.default_rng(17)
+    for seed in range(40):
+        m = int(rng.integers(1, 9))
+        cap_hi = int(rng.choice([6, 20, 127, 300]))
+        if m > 4 and cap_hi > 127:
+            cap_hi = 127
+        inst = synth.random_instance(int(rng.integers(3, 40)), m, seed=seed,
+                                     cap_lo=max(1, cap_hi // 3), cap_hi=cap_hi,
+                                     max_dur=int(rng.choice([3, 10, 40])),
+                                     demand_density=float(rng.choice([0.3, 1.0])))
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(60)])
+        for mode in (0, 1):
+            want_c, want_s = oracle.evaluate_batch(inst, orders, mode)
+            got_c, got_s = device.eval_batch(inst, orders, mode, group=int(rng.choice(GROUPS)))
+            assert np.array_equal(got_c, want_c), (seed, mode)
+            assert np.array_equal(got_s, want_s), (seed, mode)
+
+
+def test_filter_golden(golden, ginst):
+    for rec in golden["filter"]:
+        got = device.filter_batch(ginst[rec["instance"]], np.array([rec["order"]]), rec["delta"])
+        assert got[0].tolist() == rec["kept"], (rec["instance"], rec["delta"])
+
+
+def test_filter_fuzz_vs_oracle():
+    rng = np.random.default_rng(3)
+    for seed in range(20):
+        inst = synth.random_instance(int(rng.integers(4, 60)), 2, seed=seed)
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(20)])
+        for delta in (1, 7, 30, inst.n_activities):
+            got = device.filter_batch(inst, orders, delta)
+            moves = oracle.neighborhood(inst.n_activities, delta)
+            for b in range(len(orders)):
+                assert got[b].tolist() == oracle.filter_moves(inst, orders[b], moves).tolist()
+
+
+@pytest.mark.parametrize("group", GROUPS)
+def test_run_chunk_golden(golden, ginst, group):
+    for rec in golden["run_chunk"]:
+        inst = ginst[rec["instance"]]
+        res = device.run_chunk_batch(inst, rec["mode"], rec["delta"], np.array([rec["order"]]),
+                                     [np.array(rec["tabu_list"])], [rec["tabu_head"]],
+                                     rec["budget"], rec["adopted_cmax"], rec["start_cmax"],
+                                     rec["best_known_cmax"], rec["floor_cmax"], group=group)
+        st = res["stats"][0]
+        iters = int(st[0])
+        assert st[:7].tolist() == rec["out_stats"], (rec["instance"], rec["mode"])
+        assert res["trace"][0][:iters].tolist() == rec["out_trace"]
+        assert res["order"][0].tolist() == rec["out_order"]
+        assert res["best_order"][0].tolist() == rec["out_best_order"]
+        assert res["tabu"][0].tolist() == rec["out_tabu_list"]
+
+
+def test_run_chunk_batch_independent(ginst):
+    """Several searches in one launch give the same results as one each."""
+    inst = ginst["genr60s0"]
+    rng = np.random.default_rng(9)
+    orders = np.stack([random_topological_order(inst, rng) for _ in range(5)])
+    cm, _ = device.eval_batch(inst, orders, 1, want_starts=False)
+    T = 250
+    tl = [np.zeros((T, 2), np.int32) for _ in orders]
+    floor = critical_path_length(inst)
+    batch = device.run_chunk_batch(inst, 1, 60, orders, tl, [0] * 5, 7, 0, cm, cm + 3, floor)
+    for b in range(5):
+        want = oracle.run_chunk(inst, orders[b], tl[b], 0, 7, 0, int(cm[b]), int(cm[b]) + 3,
+                                floor, 60, 1)
+        assert batch["stats"][b][:7].tolist() == list(want["stats"])
+        assert batch["trace"][b][:int(want["stats"][0])].tolist() == want["trace"].tolist()
+
+
+def test_orchestrate_golden(golden, ginst):
+    """B = 1 full trajectories, identical to the reference."""
+    for rec in golden["orchestrate"]:
+        inst = ginst[rec["instance"]]
+        p = SearchParams.defaults_for(inst.n_activities, total_iters=rec["total_iters"],
+                                      workers=1, seed=rec["seed"], mode=EvalMode(rec["mode"]),
+                                      collect_trace=True, **rec["extra"])
+        st = orchestrate(inst, p)
+        key = (rec["instance"], rec["total_iters"], rec["mode"])
+        assert st.best_cmax == rec["best_cmax"], key
+        assert st.evaluations == rec["evaluations"], key
+        assert st.exchanges == rec["exchanges"], key
+        assert st.diversifications == rec["diversifications"], key
+        assert st.forced_tabu_picks == rec["forced_tabu_picks"], key
+        assert st.iterations == rec["iterations"], key
+        assert st.stop_reason == rec["stop_reason"], key
+        assert st.critical_path == rec["critical_path"], key
+        assert [t.tolist() for t in st.traces] == rec["traces"], key
+        assert st.schedule.starts.tolist() == rec["starts"], key
+        assert st.feasible
+
+
+def test_orchestrate_batch_equals_single(ginst):
+    """B = 1 per instance inside a mixed-mode batch == each solved alone (oracle)."""
+    names = ["genr30s0", "genr30s1", "example12", "fuzz3", "genr60s0"]
+    insts = [ginst[k] for k in names]
+    modes = [EvalMode.TIME, EvalMode.CAPACITY, EvalMode.TIME, EvalMode.CAPACITY, EvalMode.TIME]
+    p = SearchParams(total_iters=150, workers=1, delta=30, tabu_size=60, seed=4,
+                     collect_trace=True)
+    out = orchestrate_batch(insts, p, modes)
+    for inst, mode, run in zip(insts, modes, out.runs):
+        want = oracle.orchestrate(inst, 150, 1, 4, int(mode), delta=30, tabu_size=60,
+                                  collect_trace=True)
+        assert run.best_cmax == want["best_cmax"]
+        assert run.evaluations == want["evaluations"]
+        assert [t.tolist() for t in run.traces] == [t.tolist() for t in want["traces"]]
+
+
+def test_pool_init_matches_oracle(ginst):
+    for name, mode in (("genr30s0", 1), ("example12", 0), ("genr120s0", 1)):
+        inst = ginst[name]
+        p = SearchParams.defaults_for(inst.n_activities, pool_size=16, seed=4)
+        counters: dict = {}
+        ws = initialize_working_set(inst, p, np.random.default_rng(4), EvalMode(mode),
+                                    critical_path_length(inst), counters)
+        rng = np.random.default_rng(4)
+        evals = 0
+        for i, e in enumerate(ws.entries):
+            raw = initial_order(inst, True, rng)
+            if i % 2 == 0:
+                fo, _, _, ev = oracle.fbi(inst, raw, mode)
+                evals += ev
+            else:
+                fo = raw
+            assert e.order.tolist() == fo.tolist(), (name, i)
+            assert e.cmax == int(oracle.evaluate_batch(inst, fo[None], mode)[0][0])
+            evals += 1
+        assert counters["evaluations"] == evals
+
+
+def test_diversify_golden(golden, ginst):
+    from paper_1711_04556_b200 import diversify
+    for rec in golden["diversify"]:
+        rng = np.random.default_rng(rec["seed"])
+        out = diversify(np.array(rec["order"]), rec["phi_steps"], ginst[rec["instance"]], rng)
+        assert out.tolist() == rec["out"]
+        # the caller's rng continues exactly like numpy's after the same draws
+        ref = np.random.default_rng(rec["seed"])
+        st = oracle.rng_state(rec["seed"])
+        oracle.diversify(ginst[rec["instance"]], rec["order"], rec["phi_steps"], st)
+        assert rng.integers(1 << 30) == oracle.pcg_integers(st, 1 << 30)
+        del ref
+
+
+def test_rng_probe_golden(golden):
+    for rec in golden["rng"]:
+        ops = [(0, n) if kind == "int" else (1, n) for kind, n, _ in rec["seq"]]
+        out, _ = device.rng_probe(device.rng_words(rec["seed"]), ops)
+        flat = []
+        for kind, _, want in rec["seq"]:
+            flat.extend([want] if kind == "int" else want)
+        assert out.tolist() == flat
+
+
+def test_eq8_probe(golden):
+    quads = np.array([[c, ic, bi, best] for c, ic, bi, best, _ in golden["assigned_iterations"]])
+    got = device.eq8_probe(quads)
+    assert got.tolist() == [w for *_, w in golden["assigned_iterations"]]
+    # a dense grid against the host double-precision formula
+    import math
+    rng = np.random.default_rng(1)
+    q = np.stack([rng.integers(50, 400, 20000), rng.integers(0, 30000, 20000),
+                  rng.integers(1, 12000, 20000), np.zeros(20000, np.int64)], 1)
+    q[:, 3] = q[:, 0] - rng.integers(0, 30, 20000)
+    q[:, 3] = np.maximum(q[:, 3], 1)
+    got = device.eq8_probe(q)
+    want = [math.floor((bi / 5.0) * (0.8 * math.exp(-100.0 * (c / b - 1.0))
+                                     + 0.2 * math.exp(-4.0 * (ic / bi))))
+            for c, ic, bi, b in q.tolist()]
+    assert got.tolist() == want
+
+
+def test_edge_cases(ginst):
+    ex = ginst["example12"]
+    st = orchestrate(ex, SearchParams.defaults_for(12, total_iters=0, workers=1, seed=1))
+    assert st.iterations == 0 and st.feasible
+    chain = chain_instance([2, 2, 2, 2])
+    st = orchestrate(chain, SearchParams.defaults_for(6, total_iters=50, workers=1, seed=1,
+                                                      collect_trace=True))
+    want = oracle.orchestrate(chain, 50, 1, 1, 1, collect_trace=True)
+    assert st.evaluations == want["evaluations"] and st.best_cmax == want["best_cmax"]
+    roomy = ginst["roomy"]
+    st = orchestrate(roomy, SearchParams.defaults_for(12, total_iters=5000, workers=4, seed=2))
+    assert st.best_cmax == critical_path_length(roomy) and st.stop_reason == "critical_path"
+
+
+def test_multi_worker_solve(ginst):
+    """B > 1 CTAs share one working set: budget accounting and feasibility."""
+    inst = ginst["genr60s0"]
+    for workers in (2, 8):
+        st = orchestrate(inst, SearchParams.defaults_for(inst.n_activities, total_iters=400,
+                                                         workers=workers, seed=3))
+        assert st.iterations == 400
+        assert st.best_cmax >= critical_path_length(inst)
+        assert st.feasible and st.exchanges >= workers
+        assert st.evaluations > 400
