@@ -57,7 +57,8 @@ template <int MODE, int G, int W>
 __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob,
                                                     const int* __restrict__ orders, int batch,
                                                     int reverse, int* __restrict__ cmax,
-                                                    int* __restrict__ starts, int* err) {
+                                                    int* __restrict__ starts, int cap_lanes,
+                                                    int* err) {
   extern __shared__ __align__(16) int smem[];
   SInst I;
   const int used = align4(stage_instance(blob, smem, I));
@@ -85,13 +86,14 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
                                         active, err);
     if (active && lane_g == 0) cmax[b] = cm;
   } else {
+    const int L = cap_lanes;
     const int words = cap_thread_words(n, I.m, I.rmax) + n;
-    int* st = scratch + warp * 32 * words;
-    int* ord = st + cap_thread_words(n, I.m, I.rmax) * 32;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-    for (int p = 0; p < n; ++p) ord[p * 32 + lane] = orders[static_cast<size_t>(b) * n + p];
-    cmax[b] = sgs_cap_thread(I, st, [&](int p) { return ord[p * 32 + lane]; }, pp, pd,
+    int* st = scratch + warp * L * words;
+    int* ord = st + cap_thread_words(n, I.m, I.rmax) * L;
+    const int b = (blockIdx.x * nw + warp) * L + lane;
+    if (lane >= L || b >= batch) return;
+    for (int p = 0; p < n; ++p) ord[p * L + lane] = orders[static_cast<size_t>(b) * n + p];
+    cmax[b] = sgs_cap_thread(I, st, L, lane, [&](int p) { return ord[p * L + lane]; }, pp, pd,
                              starts ? starts + static_cast<size_t>(b) * n : nullptr);
   }
 }
@@ -239,7 +241,7 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
   } else {
     cm = 0;
     if ((threadIdx.x & 31) == 0)
-      cm = sgs_cap_thread(I, scr, [&](int p) { return ord[p]; }, pp, pd, starts);
+      cm = sgs_cap_thread(I, scr, 1, 0, [&](int p) { return ord[p]; }, pp, pd, starts);
     cm = __shfl_sync(FULL_MASK, cm, 0);
   }
   __syncwarp();
@@ -290,7 +292,7 @@ __host__ __device__ inline int pool_entry_words(int mode, int n, int m, int H, i
                                                 int rmax) {
   const int inst = (inst_smem_words(n, m, e, W) + 3) & ~3;
   const int arrays = 8 * n;  // ord, s1, s2, key, indeg, ready, border/forder, final
-  const int ev = mode == MODE_TIME ? (H + 1) * W + n : 32 * cap_thread_words(n, m, rmax);
+  const int ev = mode == MODE_TIME ? (H + 1) * W + n : cap_thread_words(n, m, rmax);
   return inst + arrays + ev + 8;
 }
 
@@ -636,15 +638,33 @@ int read_hdr(const int32_t* dblob, Hdr& h) {
   return 0;
 }
 
-template <class Kern>
-int set_smem(Kern k, size_t bytes) {
+size_t smem_optin() {
   static int optin = -1;
   if (optin < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
-  if (bytes > static_cast<size_t>(optin))
+  return static_cast<size_t>(optin);
+}
+
+// search-kernel plan: most warps (<= want) and CAP lanes whose smem fits
+bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
+                     int T, int want_threads, SmemPlan& p, int& threads) {
+  const size_t limit = smem_optin();
+  for (threads = want_threads; threads >= 32; threads -= 32) {
+    for (int lanes = 32; lanes >= (mode == MODE_CAPACITY ? 1 : 32); --lanes) {
+      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes);
+      if (static_cast<size_t>(p.total) * 4 <= limit) return true;
+    }
+  }
+  return false;
+}
+
+template <class Kern>
+int set_smem(Kern k, size_t bytes) {
+  const size_t optin = smem_optin();
+  if (bytes > optin)
     return fail("shared memory plan of " + std::to_string(bytes) + " B exceeds the " +
                 std::to_string(optin) + " B per-CTA limit");
   return cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -690,22 +710,27 @@ int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int b
   Hdr h;
   if (read_hdr(blob, h)) return -1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int threads = 256, nw = threads / 32;
-  const int inst = (inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3;
+  const size_t limit = smem_optin();
+  const size_t inst = (inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3;
   return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
-    size_t words;
-    int blocks;
-    if (MODE == MODE_TIME) {
-      words = inst + static_cast<size_t>(nw) * (32 / G) * ((h.H + 1) * W + 2 * h.n);
-      const int per_block = nw * (32 / G);
-      blocks = (batch + per_block - 1) / per_block;
-    } else {
-      words = inst + static_cast<size_t>(nw) * 32 * (cap_thread_words(h.n, h.m, h.rmax) + h.n);
-      blocks = (batch + threads - 1) / threads;
+    // largest warp count (<= 8) and CAP lane count (<= 32) whose scratch fits
+    int nw = 8, lanes = 32;
+    size_t words = 0;
+    for (;;) {
+      if (MODE == MODE_TIME)
+        words = inst + static_cast<size_t>(nw) * (32 / G) * ((h.H + 1) * W + 2 * h.n);
+      else
+        words = inst + static_cast<size_t>(nw) * lanes * (cap_thread_words(h.n, h.m, h.rmax) + h.n);
+      if (words * 4 <= limit) break;
+      if (nw > 1) nw >>= 1;
+      else if (MODE == MODE_CAPACITY && lanes > 1) --lanes;
+      else return fail("evaluation scratch does not fit in shared memory");
     }
+    const int per_block = MODE == MODE_TIME ? nw * (32 / G) : nw * lanes;
+    const int blocks = (batch + per_block - 1) / per_block;
     auto k = k_eval_batch<MODE, G, W>;
     if (set_smem(k, words * 4)) return -1;
-    k<<<blocks, threads, words * 4, s>>>(blob, orders, batch, reverse, cmax, starts, err);
+    k<<<blocks, nw * 32, words * 4, s>>>(blob, orders, batch, reverse, cmax, starts, lanes, err);
     return launch_check("k_eval_batch");
   });
 }
@@ -737,10 +762,13 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
   if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
-    SmemPlan p = plan_smem(MODE, G, W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads / 32);
+    SmemPlan p;
+    int nt;
+    if (!fit_search_plan(MODE, G, W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads, p, nt))
+      return fail("search state does not fit in shared memory");
     auto k = k_run_chunk<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
-    k<<<batch, threads, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
+    k<<<batch, nt, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
                                           adopted, start_cmax, best_known, floor_cmax, best_orders,
                                           trace, trace_cap, reinterpret_cast<long long*>(stats),
                                           moves_buf, cmax_buf, nbhd_max, p, err);
@@ -792,14 +820,17 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words),
                   [&]<int MODE, int G, int W>() -> int {
-    SmemPlan p = plan_smem(MODE, G, W, static_cast<int>(A.n_max), static_cast<int>(A.m_max),
-                           static_cast<int>(A.h_max), static_cast<int>(A.e_max),
-                           static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
-                           static_cast<int>(A.tabu_size), threads / 32);
+    SmemPlan p;
+    int nt;
+    if (!fit_search_plan(MODE, G, W, static_cast<int>(A.n_max), static_cast<int>(A.m_max),
+                         static_cast<int>(A.h_max), static_cast<int>(A.e_max),
+                         static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
+                         static_cast<int>(A.tabu_size), threads, p, nt))
+      return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
     const int grid = n_ids * static_cast<int>(A.workers);
-    k<<<grid, threads, p.total * 4, s>>>(A, inst_ids, p);
+    k<<<grid, nt, p.total * 4, s>>>(A, inst_ids, p);
     return launch_check("k_solve");
   });
 }

@@ -40,6 +40,7 @@ struct CtaCtx {
   int* scal;       // [SC_WORDS]
   int* evs;        // evaluation scratch (per warp)
   int warp_words;  // evaluation scratch words per warp
+  int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
   uint32_t* moves_buf;  // global [nbhd] compacted moves
   int* cmax_buf;        // global [nbhd] makespans
   int* err;
@@ -258,14 +259,17 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
       if (active && (lane & (G - 1)) == 0) c.cmax_buf[idx] = cm;
     }
   } else {
+    const int lanes = c.cap_lanes;
     int* st = c.evs + warp * c.warp_words;
-    for (int idx = threadIdx.x; idx < n_feas; idx += blockDim.x) {
-      const uint32_t mv = c.moves_buf[idx];
-      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
-      const int au = base[v], av = base[u];
-      c.cmax_buf[idx] = sgs_cap_thread(
-          c.I, st, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, c.I.sptr,
-          c.I.sdat, nullptr);
+    if (lane < lanes) {
+      for (int idx = warp * lanes + lane; idx < n_feas; idx += nw * lanes) {
+        const uint32_t mv = c.moves_buf[idx];
+        const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+        const int au = base[v], av = base[u];
+        c.cmax_buf[idx] = sgs_cap_thread(
+            c.I, st, lanes, lane, [&](int p) { return p == u ? au : (p == v ? av : base[p]); },
+            c.I.sptr, c.I.sdat, nullptr);
+      }
     }
   }
   __syncthreads();
@@ -285,8 +289,8 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
     } else {
       cm = 0;
       if (lane == 0)
-        cm = sgs_cap_thread(c.I, c.evs, [&](int p) { return ord[p]; }, c.I.sptr, c.I.sdat,
-                            nullptr);
+        cm = sgs_cap_thread(c.I, c.evs, c.cap_lanes, 0, [&](int p) { return ord[p]; }, c.I.sptr,
+                            c.I.sdat, nullptr);
     }
     if (lane == 0) c.scal[SC_START] = cm;
   }
@@ -408,17 +412,18 @@ __device__ void cta_diversify(CtaCtx& c, int* work, int steps, Pcg64& rng) {
 
 struct SmemPlan {
   int inst, base, pos, msp, mpp, rs, best, rowc, tabu_list, tabu_cnt, red, scal, evs;
-  int warp_words, total;
+  int warp_words, total, cap_lanes;
 };
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
-                                               int rmax) {
+                                               int rmax, int cap_lanes) {
   if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + n);
-  return 32 * cap_thread_words(n, m, rmax);
+  return cap_lanes * cap_thread_words(n, m, rmax);
 }
 
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,
-                                              int rmax, int delta, int T, int nwarps) {
+                                              int rmax, int delta, int T, int nwarps,
+                                              int cap_lanes = 32) {
   SmemPlan p;
   auto a4 = [](int x) { return (x + 3) & ~3; };
   int off = 0;
@@ -434,7 +439,8 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.tabu_cnt = off; off += a4((n * (delta + 1) + 1) / 2);
   p.red = off; off += 72;
   p.scal = off; off += SC_WORDS;
-  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax));
+  p.cap_lanes = cap_lanes;
+  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes));
   p.evs = off; off += p.warp_words * nwarps;
   p.total = off;
   return p;
@@ -459,6 +465,7 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.scal = smem + p.scal;
   c.evs = smem + p.evs;
   c.warp_words = p.warp_words;
+  c.cap_lanes = p.cap_lanes;
   c.moves_buf = moves_buf;
   c.cmax_buf = cmax_buf;
   c.err = err;

@@ -172,20 +172,21 @@ __device__ __forceinline__ int sgs_time_group(const SInst& I, uint32_t* __restri
 }
 
 // Capacity-indexed SGS, one thread per schedule.
-//   st: this warp's interleaved scratch base; word j of lane l at st[j*32+l]
+//   st: the warp's interleaved scratch; word j of slot `slot` at st[j*SK + slot]
+//       (SK = lanes sharing the scratch, 32 normally: conflict-free)
 //       layout: c[m*rmax] | copy_buf[rmax] | es[n]
 template <class ActFn>
-__device__ __forceinline__ int sgs_cap_thread(const SInst& I, int* __restrict__ st, ActFn act_at,
+__device__ __forceinline__ int sgs_cap_thread(const SInst& I, int* __restrict__ st, int SK,
+                                              int slot, ActFn act_at,
                                               const int* __restrict__ push_ptr,
                                               const int* __restrict__ push_dat,
                                               int* __restrict__ starts_out) {
-  const int lane = threadIdx.x & 31;
   const int n = I.n, m = I.m, R = I.rmax;
-  int* c = st + lane;                 // c[(k*R + i)*32]
-  int* cb = st + (m * R) * 32 + lane;  // cb[i*32]
-  int* es = cb + R * 32;              // es[a*32]
-  for (int j = 0; j < m * R; ++j) c[j * 32] = 0;
-  for (int a = 0; a < n; ++a) es[a * 32] = 0;
+  int* c = st + slot;                 // c[(k*R + i)*SK]
+  int* cb = st + (m * R) * SK + slot;  // cb[i*SK]
+  int* es = cb + R * SK;              // es[a*SK]
+  for (int j = 0; j < m * R; ++j) c[j * SK] = 0;
+  for (int a = 0; a < n; ++a) es[a * SK] = 0;
   int cmax = 0;
   for (int pos = 0; pos < n; ++pos) {
     const int act = act_at(pos);
@@ -195,31 +196,31 @@ __device__ __forceinline__ int sgs_cap_thread(const SInst& I, int* __restrict__ 
     int es_res = 0;
     for (int k = 0; k < m; ++k) {
       const int req = dem[k];
-      if (req > 0) es_res = max(es_res, c[(k * R + I.cap[k] - req) * 32]);
+      if (req > 0) es_res = max(es_res, c[(k * R + I.cap[k] - req) * SK]);
     }
-    const int start = max(es[act * 32], es_res);
+    const int start = max(es[act * SK], es_res);
     // Alg. 4 (kernels.py:81-110), quirks preserved
     for (int k = 0; k < m; ++k) {
       const int req = dem[k];
       int effort = req * dur;
       if (effort <= 0) continue;
-      int* ck = c + (k * R) * 32;
+      int* ck = c + (k * R) * SK;
       const int capk = I.cap[k];
       int copy_idx = 0;
       int new_time = start + dur;
       for (int res_idx = 0; effort > 0 && res_idx < capk; ++res_idx) {
-        const int cv = ck[res_idx * 32];
+        const int cv = ck[res_idx * SK];
         if (cv < new_time) {
-          if (copy_idx >= req) new_time = cb[(copy_idx - req) * 32];
+          if (copy_idx >= req) new_time = cb[(copy_idx - req) * SK];
           const int fl = cv < start ? start : cv;
           const int diff = new_time - fl;
           if (effort - diff > 0) {
             effort -= diff;
-            cb[copy_idx * 32] = cv;
+            cb[copy_idx * SK] = cv;
             ++copy_idx;
-            ck[res_idx * 32] = new_time;
+            ck[res_idx * SK] = new_time;
           } else {
-            ck[res_idx * 32] = fl + effort;
+            ck[res_idx * SK] = fl + effort;
             effort = 0;
           }
         }
@@ -229,7 +230,7 @@ __device__ __forceinline__ int sgs_cap_thread(const SInst& I, int* __restrict__ 
     cmax = max(cmax, fin);
     for (int e = push_ptr[act]; e < push_ptr[act + 1]; ++e) {
       const int s = push_dat[e];
-      if (es[s * 32] < fin) es[s * 32] = fin;
+      if (es[s * SK] < fin) es[s * SK] = fin;
     }
     if (starts_out) starts_out[act] = start;
   }
