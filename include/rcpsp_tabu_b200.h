@@ -150,6 +150,10 @@ int rcpsp_diversify_batch(const int32_t *blob, int32_t *orders, int batch, int p
  * cooperation.py:233-243). ops: [k*2] (kind, n) with kind 0 = integers(n),
  * 1 = permutation(arange(n)); out receives the draws back to back. */
 int rcpsp_rng_probe(uint64_t *state, const int32_t *ops, int k, int32_t *out, void *stream);
+/* Shared-memory bandwidth microbenchmark (the roofline denominator of the
+ * on-chip-bound search kernel): blocks x threads stream iters x 64 bytes each
+ * out of a 32 KB shared array; the caller times it with CUDA events. */
+int rcpsp_smem_probe(int blocks, int threads, int iters, int32_t *sink, void *stream);
 int rcpsp_eq8_probe(const int64_t *quad /*[k*4] cmax, ic, block_iters, best*/, int k,
                     int64_t *out, void *stream);
 

@@ -202,6 +202,25 @@ __global__ void k_eq8_probe(const long long* quad, int k, long long* out) {
   if (i < k) out[i] = eq8(quad[4 * i], quad[4 * i + 1], quad[4 * i + 2], quad[4 * i + 3]);
 }
 
+// Shared-memory bandwidth probe (roofline denominator): every thread streams
+// 128-bit loads over a 32 KB shared array; bytes = threads * iters * 64.
+__global__ void __launch_bounds__(1024) k_smem_probe(int iters, int* sink) {
+  __shared__ __align__(16) int4 buf[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_int4(i, i + 1, i + 2, i + 3);
+  __syncthreads();
+  int4 acc = make_int4(0, 0, 0, 0);
+  int idx = threadIdx.x & 2047;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int4 v = buf[(idx + j * 32) & 2047];
+      acc.x ^= v.x; acc.y += v.y; acc.z ^= v.z; acc.w += v.w;
+    }
+    idx = (idx + 128 + (acc.x & 1)) & 2047;
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x7fffffff) sink[0] = 1;
+}
+
 // =========================================================================
 // K0: working-set initialisation
 
@@ -861,6 +880,11 @@ int rcpsp_diversify_batch(const int32_t* blob, int32_t* orders, int batch, int p
   k_diversify<<<batch, 256, p.total * 4, static_cast<cudaStream_t>(stream)>>>(
       blob, orders, phi_steps, rng, p);
   return launch_check("k_diversify");
+}
+
+int rcpsp_smem_probe(int blocks, int threads, int iters, int32_t* sink, void* stream) {
+  k_smem_probe<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
+  return launch_check("k_smem_probe");
 }
 
 int rcpsp_rng_probe(uint64_t* state, const int32_t* ops, int k, int32_t* out, void* stream) {

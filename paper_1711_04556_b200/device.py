@@ -306,6 +306,26 @@ def eq8_probe(quads: np.ndarray) -> np.ndarray:
     return out.cpu().numpy()
 
 
+def smem_bandwidth(iters: int = 4096, reps: int = 5) -> float:
+    """Measured shared-memory load bandwidth of this GPU in GB/s (best of reps)."""
+    torch = _torch()
+    L = _native.lib()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads = sms * 2, 1024
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    best = 0.0
+    for r in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        check(L.rcpsp_smem_probe(blocks, threads, iters, ptr(sink), stream_handle()),
+              "rcpsp_smem_probe")
+        e1.record()
+        e1.synchronize()
+        if r:
+            best = max(best, blocks * threads * iters * 64 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
 DEV_ERRORS = {1: "bad instance blob", 2: "no resource window before the horizon "
               "(demand above capacity?)", 3: "shared memory plan", 4: "tabu move outside the "
               "delta band", 5: "precedence cycle", 6: "bad move"}
