@@ -37,9 +37,17 @@ __device__ __forceinline__ void set_err(int* err, int code) {
 }
 
 // Shared-memory view of one instance.  All arrays are int32 / uint32.
+// Per-activity record of the TIME evaluator (one LDS.128 per activity):
+//   x = duration, y = packed demand word 0,
+//   z = push span: first edge | (edge count << 16) of the graph finish times
+//       propagate along (successors forward, predecessors for the reversed
+//       project), w = the doubling shifts of the run-of-`dur` window test
+//       (5 fields of 6 bits, see window_shifts).
 struct SInst {
   int n, m, H, e, W, rmax, cpm;
   uint32_t hi;           // high bit of every packed resource lane (TIME fits test)
+  const int4* info_f;    // [n] forward records
+  const int4* info_r;    // [n] reversed-project records
   const int* dur;        // [n]
   const uint32_t* req;   // [n*W] packed per-resource demands (TIME)
   const int* dem;        // [n*m] row-major demands (CAP)
@@ -52,7 +60,19 @@ struct SInst {
 };
 
 __host__ __device__ __forceinline__ int inst_smem_words(int n, int m, int e, int W) {
-  return n + n * W + n * m + m + W + 2 * (n + 1) + 2 * e;
+  return 8 * n + n + n * W + n * m + m + W + 2 * (n + 1) + 2 * e;
+}
+
+// y &= y >> s_i (i = 1..5) turns a slot mask into "a run of d ones starts
+// here" (d <= 32): s_i = min(acc, d - acc), acc += s_i, acc starting at 1.
+__host__ __device__ __forceinline__ int window_shifts(int d) {
+  int packed = 0, acc = 1;
+  for (int i = 0; i < 5; ++i) {
+    const int s = d > acc ? (acc < d - acc ? acc : d - acc) : 0;
+    packed |= s << (6 * i);
+    acc += s;
+  }
+  return packed;
 }
 
 // Stage a blob into shared memory (all threads of the CTA call this; the
@@ -67,7 +87,21 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
   I.cpm = blob[B_CPM];
   I.hi = blob[B_LB] == 8 ? 0x80808080u : 0x80008000u;
   const int n = I.n, m = I.m, e = I.e, W = I.W;
-  int* p = smem;
+  int4* inf = reinterpret_cast<int4*>(smem);  // smem base is 16-byte aligned
+  {
+    const int* bd = blob + blob[B_OFF_DUR];
+    const int* br = blob + blob[B_OFF_REQ];
+    const int* sp = blob + blob[B_OFF_SPTR];
+    const int* pp = blob + blob[B_OFF_PPTR];
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+      const int d = bd[a], r = br[a * W], sh = window_shifts(d);
+      inf[a] = make_int4(d, r, sp[a] | ((sp[a + 1] - sp[a]) << 16), sh);
+      inf[n + a] = make_int4(d, r, pp[a] | ((pp[a + 1] - pp[a]) << 16), sh);
+    }
+  }
+  I.info_f = inf;
+  I.info_r = inf + n;
+  int* p = smem + 8 * n;
   auto copy = [&](int off, int cnt) -> int* {
     int* dst = p;
     const int* src = blob + off;

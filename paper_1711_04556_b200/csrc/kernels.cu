@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
                                                     int reverse, int* __restrict__ cmax,
                                                     int* __restrict__ starts, int cap_lanes,
                                                     int* err) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   SInst I;
   const int used = align4(stage_instance(blob, smem, I));
   __syncthreads();
@@ -81,9 +81,19 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
       for (int p = lane_g; p < n; p += G) ord[p] = orders[static_cast<size_t>(b) * n + p];
     __syncwarp();
     if (!__any_sync(FULL_MASK, active)) return;
-    const int cm = sgs_time_group<G, W>(I, tau, es, [&](int p) { return ord[p]; }, pp, pd,
-                                        starts ? starts + static_cast<size_t>(b) * n : nullptr,
-                                        active, err);
+    int cm;
+    if constexpr (G == 32) {
+      if (!active) return;
+      cm = sgs_time_warp<W>(reverse ? I.info_r : I.info_f, pd, I.req, I.capw[0],
+                            W == 2 ? I.capw[1] : 0u, I.hi, n, I.H, tau, es,
+                            [&](int p) { return ord[p]; },
+                            starts ? starts + static_cast<size_t>(b) * n : nullptr, err);
+    } else {
+      cm = sgs_time_group<G, W>(I, tau, es, [&](int p) { return ord[p]; },
+                                reverse ? I.info_r : I.info_f, pd,
+                                starts ? starts + static_cast<size_t>(b) * n : nullptr, active,
+                                err);
+    }
     if (active && lane_g == 0) cmax[b] = cm;
   } else {
     const int L = cap_lanes;
@@ -102,12 +112,12 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
 // K2: stand-alone run_chunk (parity / kernels.run_chunk drop-in)
 
 template <int MODE, int G, int W>
-__global__ void __launch_bounds__(512) k_run_chunk(
+__global__ void __launch_bounds__(512, 2) k_run_chunk(
     const int* __restrict__ blob, int delta, int T, int* orders, uint32_t* tabu, int* heads,
     const int* budget, const int* adopted, const int* start_cmax, const int* best_known,
     int floor_cmax, int* best_orders, int* trace, int trace_cap, long long* stats,
     uint32_t* moves_buf, int* cmax_buf, int nbhd_max, SmemPlan plan, int* err) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   const int b = blockIdx.x;
   CtaCtx c;
   cta_setup(c, blob, smem, plan, delta, T, moves_buf + static_cast<size_t>(b) * nbhd_max,
@@ -143,7 +153,7 @@ __global__ void __launch_bounds__(512) k_run_chunk(
 __global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ blob, const int* orders,
                                                       int delta, uint32_t* out_moves, int nbhd_cap,
                                                       int* out_count, SmemPlan plan) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   const int b = blockIdx.x;
   CtaCtx c;
   cta_setup(c, blob, smem, plan, delta, 1, out_moves + static_cast<size_t>(b) * nbhd_cap, nullptr,
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ bl
 
 __global__ void __launch_bounds__(256) k_diversify(const int* __restrict__ blob, int* orders, int steps,
                                                    uint64_t* rng_words, SmemPlan plan) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   const int b = blockIdx.x;
   CtaCtx c;
   cta_setup(c, blob, smem, plan, 1, 1, nullptr, nullptr, nullptr);
@@ -255,8 +265,11 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
   const int* pd = reverse ? I.pdat : I.sdat;
   int cm;
   if constexpr (MODE == MODE_TIME) {
-    cm = sgs_time_group<32, W>(I, reinterpret_cast<uint32_t*>(scr), scr + (I.H + 1) * W,
-                               [&](int p) { return ord[p]; }, pp, pd, starts, true, err);
+    cm = sgs_time_warp<W>(reverse ? I.info_r : I.info_f, pd, I.req, I.capw[0],
+                          W == 2 ? I.capw[1] : 0u, I.hi, I.n, I.H,
+                          reinterpret_cast<uint32_t*>(scr), scr + (I.H + 1) * W,
+                          [&](int p) { return ord[p]; }, starts, err); }, reverse ? I.info_r : I.info_f, pd,
+                               starts, true, err);
   } else {
     cm = 0;
     if ((threadIdx.x & 31) == 0)
@@ -319,7 +332,7 @@ __host__ __device__ inline int pool_entry_words(int mode, int n, int m, int H, i
 // evaluation of every entry (cooperation.py:340-351); one warp per entry.
 template <int MODE, int W>
 __global__ void __launch_bounds__(32) k_pool_entry(RcpspSolveArgs A, const int* ids) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   const int slot = blockIdx.x / static_cast<int>(A.pool_size);
   const int f = blockIdx.x % static_cast<int>(A.pool_size);
   const int iid = ids[slot];
@@ -419,9 +432,9 @@ __device__ __forceinline__ int64_t ldcg64(const int64_t* p) {
 }
 
 template <int MODE, int G, int W>
-__global__ void __launch_bounds__(512) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
+__global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
                                                SmemPlan plan) {
-  extern __shared__ __align__(16) int smem[];
+  int* smem = dsm;
   const int B = static_cast<int>(A.workers);
   const int slot = blockIdx.x / B, wk = blockIdx.x % B;
   const int iid = ids[slot];

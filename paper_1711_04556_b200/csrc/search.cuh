@@ -227,50 +227,112 @@ __device__ __forceinline__ int cta_filter(CtaCtx& c) {
 }
 
 // ------------------------------------------------------------- evaluation
+//
+// The evaluation phases are __noinline__ with scalar arguments (shared
+// arrays as word offsets into the dynamic shared memory `dsm`), so the hot
+// loops get their own register allocation, independent of the exchange /
+// selection code around them, and every shared access stays an LDS/STS.
+
+extern __shared__ __align__(16) int dsm[];
+
+__device__ __forceinline__ int soff(const void* p) {
+  return static_cast<int>(reinterpret_cast<const int*>(p) - dsm);
+}
+
+// TIME, one warp per schedule
+template <int W>
+__device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req, int o_base,
+                                               int o_evs, uint32_t cap0, uint32_t cap1,
+                                               uint32_t hi, int n, int H,
+                                               const uint32_t* __restrict__ moves,
+                                               int* __restrict__ cmax_out, int n_feas,
+                                               int warp_words, int* err) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int4* info = reinterpret_cast<const int4*>(dsm + o_info);
+  const int* sdat = dsm + o_sdat;
+  const uint32_t* req = reinterpret_cast<const uint32_t*>(dsm + o_req);
+  const int* base = dsm + o_base;
+  uint32_t* tau = reinterpret_cast<uint32_t*>(dsm + o_evs + warp * warp_words);
+  int* es = dsm + o_evs + warp * warp_words + (H + 1) * W;
+  for (int idx = warp; idx < n_feas; idx += nw) {
+    const uint32_t mv = moves[idx];
+    const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    const int au = base[v], av = base[u];
+    const int cm = sgs_time_warp<W>(
+        info, sdat, req, cap0, cap1, hi, n, H, tau, es,
+        [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, nullptr, err);
+    if (lane == 0) cmax_out[idx] = cm;
+  }
+}
+
+// TIME, G < 32 lanes per schedule
+template <int G, int W>
+__device__ __noinline__ void eval_moves_timeg(const SInst& I, int o_base, int o_evs,
+                                              const uint32_t* __restrict__ moves,
+                                              int* __restrict__ cmax_out, int n_feas,
+                                              int warp_words, int* err) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int S = 32 / G;
+  const int grp = lane / G;
+  const int gid = warp * S + grp;
+  const int ngroups = nw * S;
+  const int gwords = (I.H + 1) * W + I.n;
+  const int* base = dsm + o_base;
+  uint32_t* tau = reinterpret_cast<uint32_t*>(dsm + o_evs + warp * warp_words + grp * gwords);
+  int* es = reinterpret_cast<int*>(tau) + (I.H + 1) * W;
+  for (int b = 0; b < n_feas; b += ngroups) {
+    const int idx = b + gid;
+    const bool active = idx < n_feas;
+    if (!__any_sync(FULL_MASK, active)) break;
+    int u = -1, v = -1, au = 0, av = 0;
+    if (active) {
+      const uint32_t mv = moves[idx];
+      u = static_cast<int>(mv >> 16);
+      v = static_cast<int>(mv & 0xffff);
+      au = base[v];
+      av = base[u];
+    }
+    const int cm = sgs_time_group<G, W>(
+        I, tau, es, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, I.info_f,
+        I.sdat, nullptr, active, err);
+    if (active && (lane & (G - 1)) == 0) cmax_out[idx] = cm;
+  }
+}
+
+// CAP, one thread per schedule
+__device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_evs,
+                                            const uint32_t* __restrict__ moves,
+                                            int* __restrict__ cmax_out, int n_feas,
+                                            int warp_words, int lanes) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int* base = dsm + o_base;
+  int* st = dsm + o_evs + warp * warp_words;
+  if (lane >= lanes) return;
+  for (int idx = warp * lanes + lane; idx < n_feas; idx += nw * lanes) {
+    const uint32_t mv = moves[idx];
+    const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    const int au = base[v], av = base[u];
+    cmax_out[idx] = sgs_cap_thread(
+        I, st, lanes, lane, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, I.sptr,
+        I.sdat, nullptr);
+  }
+}
 
 // every compacted move -> cmax_buf (full SGS of the swapped order)
 template <int MODE, int G, int W>
 __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int* base = c.base;
   if constexpr (MODE == MODE_TIME) {
-    constexpr int S = 32 / G;
-    const int grp = lane / G;
-    const int gid = warp * S + grp;
-    const int ngroups = nw * S;
-    const int gwords = (c.I.H + 1) * W + c.I.n;
-    uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs + warp * c.warp_words + grp * gwords);
-    int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
-    for (int b = 0; b < n_feas; b += ngroups) {
-      const int idx = b + gid;
-      const bool active = idx < n_feas;
-      if (!__any_sync(FULL_MASK, active)) break;
-      int u = -1, v = -1, au = 0, av = 0;
-      if (active) {
-        const uint32_t mv = c.moves_buf[idx];
-        u = static_cast<int>(mv >> 16);
-        v = static_cast<int>(mv & 0xffff);
-        au = base[v];
-        av = base[u];
-      }
-      const int cm = sgs_time_group<G, W>(
-          c.I, tau, es, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, c.I.sptr,
-          c.I.sdat, nullptr, active, c.err);
-      if (active && (lane & (G - 1)) == 0) c.cmax_buf[idx] = cm;
+    if constexpr (G == 32) {
+      eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
+                           soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
+                           c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
+    } else {
+      eval_moves_timeg<G, W>(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
+                             c.warp_words, c.err);
     }
   } else {
-    const int lanes = c.cap_lanes;
-    int* st = c.evs + warp * c.warp_words;
-    if (lane < lanes) {
-      for (int idx = warp * lanes + lane; idx < n_feas; idx += nw * lanes) {
-        const uint32_t mv = c.moves_buf[idx];
-        const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
-        const int au = base[v], av = base[u];
-        c.cmax_buf[idx] = sgs_cap_thread(
-            c.I, st, lanes, lane, [&](int p) { return p == u ? au : (p == v ? av : base[p]); },
-            c.I.sptr, c.I.sdat, nullptr);
-      }
-    }
+    eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
+                   c.warp_words, c.cap_lanes);
   }
   __syncthreads();
 }
@@ -284,8 +346,9 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
     if constexpr (MODE == MODE_TIME) {
       uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
       int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
-      cm = sgs_time_group<G, W>(c.I, tau, es, [&](int p) { return ord[p]; }, c.I.sptr, c.I.sdat,
-                                nullptr, lane < G, c.err);
+      cm = sgs_time_warp<W>(c.I.info_f, c.I.sdat, c.I.req, c.I.capw[0],
+                            W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, tau, es,
+                            [&](int p) { return ord[p]; }, nullptr, c.err);
     } else {
       cm = 0;
       if (lane == 0)

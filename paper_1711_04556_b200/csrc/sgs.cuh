@@ -32,140 +32,215 @@ __device__ __forceinline__ bool fits1(uint32_t w, uint32_t r, uint32_t hi) {
   return (((w | hi) - r) & hi) == hi;
 }
 
-template <int W>
-struct Req {
-  uint32_t r[W];
-};
-
 // Time-indexed SGS for one schedule per G-lane group.
-//   tau:   group's profile, (H+1)*W words, slot t at tau[t*W + w]
-//   es:    group's [n] earliest-start scratch
+//   tau:   the group's profile, (H+1)*W words, slot t at tau[t*W + w]
+//   es:    the group's [n] earliest-start scratch
 //   act_at(pos) -> activity at position pos (group-uniform)
-//   push_ptr/push_dat: graph along which finish times propagate (successors
-//     for a forward pass; predecessors for the reversed project)
+//   info / push_dat: per-activity records (common.cuh) and the edge targets
+//     finish times propagate to (I.info_f + I.sdat forward; I.info_r +
+//     I.pdat for the reversed project)
 //   starts_out: optional [n] (lane 0 of the group writes)
 // Returns the makespan (group-uniform).  `active` false: the group only
-// joins the warp-collective ballots.
+// joins the warp-collective votes.
+//
+// Per activity: record + es in two LDS; no scan when the activity needs no
+// resource, or when es is at/after the materialised profile (everything there
+// is free).  Otherwise each round tests G slots (one LDS each lane), ballots,
+// and resolves the earliest window branch-free: the carried run from the
+// previous round, else the first run of `dur` ones inside the round (five
+// precomputed doubling shifts).
 template <int G, int W, class ActFn>
 __device__ __forceinline__ int sgs_time_group(const SInst& I, uint32_t* __restrict__ tau,
                                               int* __restrict__ es, ActFn act_at,
-                                              const int* __restrict__ push_ptr,
+                                              const int4* __restrict__ info,
                                               const int* __restrict__ push_dat,
                                               int* __restrict__ starts_out, bool active,
                                               int* err) {
   const int lane = threadIdx.x & 31;
   const int lane_g = lane & (G - 1);
   const int gshift = lane & ~(G - 1) & 31;
-  const uint32_t GM = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
+  constexpr uint32_t GM = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
   const int n = I.n, H = I.H;
   const uint32_t hi = I.hi;
+  const uint32_t cap0 = I.capw[0];
+  const uint32_t cap1 = W == 2 ? I.capw[1] : 0u;
 
   if (active)
     for (int a = lane_g; a < n; a += G) es[a] = 0;
   __syncwarp();
 
-  uint32_t capw[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) capw[w] = I.capw[w];
-
   int cmax = 0;
-  int hw = 0;  // profile slots [0, hw) are materialised; >= hw are full
+  int hw = 0;  // profile slots [0, hw) are materialised; >= hw are at capacity
   for (int pos = 0; pos < n; ++pos) {
-    int act = 0, dur = 0, esv = 0;
-    bool need = false;
-    Req<W> rq;
-#pragma unroll
-    for (int w = 0; w < W; ++w) rq.r[w] = 0;
+    int4 rec = make_int4(0, 0, 0, 0);
+    int act = 0, esv = 0;
+    uint32_t r1 = 0;
     if (active) {
       act = act_at(pos);
-      dur = I.dur[act];
+      rec = info[act];
       esv = es[act];
-      uint32_t any = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        rq.r[w] = I.req[act * W + w];
-        any |= rq.r[w];
-      }
-      need = dur > 0 && any != 0;
+      if (W == 2) r1 = I.req[act * 2 + 1];
     }
+    const int dur = rec.x;
+    const uint32_t r0 = static_cast<uint32_t>(rec.y);
+    const bool need = dur > 0 && (r0 | r1) != 0;
     int start = esv;
-    // window scan (kernels.py:117-136): first t >= es with [t, t+dur) fitting
-    bool done = !need;
+    bool done = !(need && esv < hw);
     int t0 = esv, carry = 0;
     while (__any_sync(FULL_MASK, !done)) {
       bool ok = false;
       if (!done) {
         const int t = t0 + lane_g;
-        if (t < H) {
-          if (t >= hw) {
-            ok = true;
-          } else {
-            ok = true;
-#pragma unroll
-            for (int w = 0; w < W; ++w) ok = ok && fits1(tau[t * W + w], rq.r[w], hi);
-          }
+        uint32_t w0 = cap0, w1 = cap1;
+        if (t < hw) {
+          w0 = tau[t * W];
+          if (W == 2) w1 = tau[t * W + 1];
         }
+        ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
       }
-      const uint32_t bal = __ballot_sync(FULL_MASK, ok);
+      const uint32_t m = (__ballot_sync(FULL_MASK, ok) >> gshift) & GM;
       if (!done) {
-        const uint32_t m = (bal >> gshift) & GM;
-        const int z = (m == GM) ? G : (__ffs(~m) - 1);
+        const uint32_t zm = ~m & GM;
+        const int z = zm ? __ffs(zm) - 1 : G;
+        uint32_t y = 0;
+        if (dur <= G) {
+          const int sh = rec.w;
+          y = m;
+          y &= y >> (sh & 63);
+          y &= y >> ((sh >> 6) & 63);
+          y &= y >> ((sh >> 12) & 63);
+          y &= y >> ((sh >> 18) & 63);
+          y &= y >> ((sh >> 24) & 63);
+        }
         if (carry + z >= dur) {
           start = t0 - carry;
           done = true;
-        } else if (z == G) {
-          carry += G;
-        } else {
-          uint32_t y = 0;
-          if (dur <= G) {
-            y = m;
-            int k = 1;
-            while (2 * k <= dur) {
-              y &= y >> k;
-              k <<= 1;
-            }
-            if (k < dur) y &= y >> (dur - k);
-          }
-          if (y) {
-            start = t0 + __ffs(y) - 1;
-            done = true;
-          } else {
-            carry = __clz(~(m << (32 - G)));
-          }
-        }
-        t0 += G;
-        if (!done && t0 >= H) {  // cannot happen for valid instances
-          start = H;
+        } else if (y) {
+          start = t0 + __ffs(y) - 1;
           done = true;
-          if (lane_g == 0) set_err(err, DE_NO_WINDOW);
+        } else {
+          carry = zm ? __clz(~(m << (32 - G))) : carry + G;
+          t0 += G;
+          if (t0 >= H) {  // cannot happen for valid instances
+            start = H;
+            done = true;
+            if (lane_g == 0) set_err(err, DE_NO_WINDOW);
+          }
         }
       }
     }
     if (active) {
       const int fin = start + dur;
       if (need) {
-        // materialise [hw, start) at full capacity, subtract on [start, fin)
+        // materialise [hw, start) at capacity, subtract the demand on [start, fin)
         for (int t = hw + lane_g; t < start; t += G) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) tau[t * W + w] = capw[w];
+          tau[t * W] = cap0;
+          if (W == 2) tau[t * W + 1] = cap1;
         }
         for (int t = start + lane_g; t < fin; t += G) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            const uint32_t v = (t >= hw) ? capw[w] : tau[t * W + w];
-            tau[t * W + w] = v - rq.r[w];
-          }
+          const bool old = t < hw;
+          tau[t * W] = (old ? tau[t * W] : cap0) - r0;
+          if (W == 2) tau[t * W + 1] = (old ? tau[t * W + 1] : cap1) - r1;
         }
         hw = max(hw, fin);
       }
       cmax = max(cmax, fin);
-      const int e0 = push_ptr[act], e1 = push_ptr[act + 1];
-      for (int e = e0 + lane_g; e < e1; e += G) {
-        const int s = push_dat[e];
+      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+      for (int e = lane_g; e < ecnt; e += G) {
+        const int s = push_dat[e0 + e];
         if (es[s] < fin) es[s] = fin;
       }
       if (starts_out && lane_g == 0) starts_out[act] = start;
     }
+    __syncwarp();
+  }
+  return cmax;
+}
+
+// Warp-uniform specialisation of sgs_time_group for G = 32 (one schedule per
+// warp): identical results, but every branch is warp-uniform (the values
+// come from ballots and broadcast loads), so the loop carries no per-lane
+// done/active state and no reconvergence barriers.
+template <int W, class ActFn>
+__device__ __forceinline__ int sgs_time_warp(const int4* __restrict__ info,
+                                             const int* __restrict__ push_dat,
+                                             const uint32_t* __restrict__ req, uint32_t cap0,
+                                             uint32_t cap1, uint32_t hi, int n, int H,
+                                             uint32_t* __restrict__ tau, int* __restrict__ es,
+                                             ActFn act_at, int* __restrict__ starts_out,
+                                             int* err) {
+  const int lane = threadIdx.x & 31;
+  for (int a = lane; a < n; a += 32) es[a] = 0;
+  __syncwarp();
+  int cmax = 0, hw = 0;
+  for (int pos = 0; pos < n; ++pos) {
+    const int act = act_at(pos);
+    const int4 rec = info[act];
+    const int esv = es[act];
+    const int dur = rec.x;
+    const uint32_t r0 = static_cast<uint32_t>(rec.y);
+    const uint32_t r1 = W == 2 ? req[act * 2 + 1] : 0u;
+    int start = esv;
+    if (dur > 0 && (r0 | r1) != 0) {
+      if (esv < hw) {
+        int t0 = esv, carry = 0;
+        for (;;) {
+          const int t = t0 + lane;
+          uint32_t w0 = cap0, w1 = cap1;
+          if (t < hw) {
+            w0 = tau[t * W];
+            if (W == 2) w1 = tau[t * W + 1];
+          }
+          const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
+          const uint32_t m = __ballot_sync(FULL_MASK, ok);
+          const uint32_t zm = ~m;
+          const int z = zm ? __ffs(zm) - 1 : 32;
+          if (carry + z >= dur) {
+            start = t0 - carry;
+            break;
+          }
+          if (dur <= 32) {
+            const int sh = rec.w;
+            uint32_t y = m;
+            y &= y >> (sh & 63);
+            y &= y >> ((sh >> 6) & 63);
+            y &= y >> ((sh >> 12) & 63);
+            y &= y >> ((sh >> 18) & 63);
+            y &= y >> ((sh >> 24) & 63);
+            if (y) {
+              start = t0 + __ffs(y) - 1;
+              break;
+            }
+          }
+          carry = zm ? __clz(zm) : carry + 32;
+          t0 += 32;
+          if (t0 >= H) {  // cannot happen for valid instances
+            start = H;
+            if (lane == 0) set_err(err, DE_NO_WINDOW);
+            break;
+          }
+        }
+      }
+      const int fin = start + dur;
+      for (int t = hw + lane; t < start; t += 32) {
+        tau[t * W] = cap0;
+        if (W == 2) tau[t * W + 1] = cap1;
+      }
+      for (int t = start + lane; t < fin; t += 32) {
+        const bool old = t < hw;
+        tau[t * W] = (old ? tau[t * W] : cap0) - r0;
+        if (W == 2) tau[t * W + 1] = (old ? tau[t * W + 1] : cap1) - r1;
+      }
+      hw = max(hw, fin);
+    }
+    const int fin = start + dur;
+    cmax = max(cmax, fin);
+    const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+    for (int e = lane; e < ecnt; e += 32) {
+      const int s = push_dat[e0 + e];
+      if (es[s] < fin) es[s] = fin;
+    }
+    if (starts_out && lane == 0) starts_out[act] = start;
     __syncwarp();
   }
   return cmax;
