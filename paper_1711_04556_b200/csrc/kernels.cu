@@ -268,8 +268,7 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
     cm = sgs_time_warp<W>(reverse ? I.info_r : I.info_f, pd, I.req, I.capw[0],
                           W == 2 ? I.capw[1] : 0u, I.hi, I.n, I.H,
                           reinterpret_cast<uint32_t*>(scr), scr + (I.H + 1) * W,
-                          [&](int p) { return ord[p]; }, starts, err); }, reverse ? I.info_r : I.info_f, pd,
-                               starts, true, err);
+                          [&](int p) { return ord[p]; }, starts, err);
   } else {
     cm = 0;
     if ((threadIdx.x & 31) == 0)
