@@ -254,13 +254,16 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req
   const int* base = dsm + o_base;
   uint32_t* tau = reinterpret_cast<uint32_t*>(dsm + o_evs + warp * warp_words);
   int* es = dsm + o_evs + warp * warp_words + (H + 1) * W;
+  int* ord = es + n;
+  const uint32_t a_info = sa(info), a_push = sa(sdat), a_req = sa(req), a_tau = sa(tau),
+                 a_es = sa(es), a_ord = sa(ord);
   for (int idx = warp; idx < n_feas; idx += nw) {
     const uint32_t mv = moves[idx];
     const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
-    const int au = base[v], av = base[u];
-    const int cm = sgs_time_warp<W>(
-        info, sdat, req, cap0, cap1, hi, n, H, tau, es,
-        [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, nullptr, err);
+    for (int p = lane; p < n; p += 32) ord[p] = base[p == u ? v : (p == v ? u : p)];
+    __syncwarp();
+    const int cm = sgs_time_warp<W>(a_info, a_push, a_req, cap0, cap1, hi, n, H, a_tau, a_es,
+                                    a_ord, nullptr, err);
     if (lane == 0) cmax_out[idx] = cm;
   }
 }
@@ -346,9 +349,9 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
     if constexpr (MODE == MODE_TIME) {
       uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
       int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
-      cm = sgs_time_warp<W>(c.I.info_f, c.I.sdat, c.I.req, c.I.capw[0],
-                            W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, tau, es,
-                            [&](int p) { return ord[p]; }, nullptr, c.err);
+      cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req), c.I.capw[0],
+                            W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, sa(tau), sa(es),
+                            sa(ord), nullptr, c.err);
     } else {
       cm = 0;
       if (lane == 0)
@@ -480,7 +483,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + n);
+  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + n) + n;
   return cap_lanes * cap_thread_words(n, m, rmax);
 }
 

@@ -157,62 +157,82 @@ __device__ __forceinline__ int sgs_time_group(const SInst& I, uint32_t* __restri
   return cmax;
 }
 
-// Warp-uniform specialisation of sgs_time_group for G = 32 (one schedule per
-// warp): identical results, but every branch is warp-uniform (the values
-// come from ballots and broadcast loads), so the loop carries no per-lane
-// done/active state and no reconvergence barriers.
-template <int W, class ActFn>
-__device__ __forceinline__ int sgs_time_warp(const int4* __restrict__ info,
-                                             const int* __restrict__ push_dat,
-                                             const uint32_t* __restrict__ req, uint32_t cap0,
-                                             uint32_t cap1, uint32_t hi, int n, int H,
-                                             uint32_t* __restrict__ tau, int* __restrict__ es,
-                                             ActFn act_at, int* __restrict__ starts_out,
+// ---- explicit shared-memory access (32-bit shared addresses)
+__device__ __forceinline__ uint32_t sa(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same
+// results as sgs_time_group; every branch is warp-uniform and every shared
+// access goes through a precomputed 32-bit shared address.
+//   a_ord:  the warp's order [n] (already swapped)      a_info: records [n]
+//   a_push: edge targets of the push graph               a_req:  packed demand
+//   a_tau:  profile (H+1)*W words                        a_es:   [n] scratch
+template <int W>
+__device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, uint32_t a_req,
+                                             uint32_t cap0, uint32_t cap1, uint32_t hi, int n,
+                                             int H, uint32_t a_tau, uint32_t a_es,
+                                             uint32_t a_ord, int* __restrict__ starts_out,
                                              int* err) {
   const int lane = threadIdx.x & 31;
-  for (int a = lane; a < n; a += 32) es[a] = 0;
+  for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
   int cmax = 0, hw = 0;
   for (int pos = 0; pos < n; ++pos) {
-    const int act = act_at(pos);
-    const int4 rec = info[act];
-    const int esv = es[act];
+    const int act = static_cast<int>(lds32(a_ord + 4 * pos));
+    const int4 rec = lds128(a_info + 16 * act);
+    const int esv = static_cast<int>(lds32(a_es + 4 * act));
     const int dur = rec.x;
     const uint32_t r0 = static_cast<uint32_t>(rec.y);
-    const uint32_t r1 = W == 2 ? req[act * 2 + 1] : 0u;
+    const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
     int start = esv;
     if (dur > 0 && (r0 | r1) != 0) {
       if (esv < hw) {
+        const int sh = rec.w;
+        const int s0 = sh & 63, s1 = (sh >> 6) & 63, s2 = (sh >> 12) & 63,
+                  s3 = (sh >> 18) & 63, s4 = (sh >> 24) & 63;
         int t0 = esv, carry = 0;
         for (;;) {
           const int t = t0 + lane;
           uint32_t w0 = cap0, w1 = cap1;
           if (t < hw) {
-            w0 = tau[t * W];
-            if (W == 2) w1 = tau[t * W + 1];
+            w0 = lds32(a_tau + 4 * W * t);
+            if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
           }
           const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
           const uint32_t m = __ballot_sync(FULL_MASK, ok);
-          const uint32_t zm = ~m;
-          const int z = zm ? __ffs(zm) - 1 : 32;
-          if (carry + z >= dur) {
+          const int z = __ffs(~m) - 1;              // -1 when all 32 slots fit
+          if (carry + (z < 0 ? 32 : z) >= dur) {
             start = t0 - carry;
             break;
           }
           if (dur <= 32) {
-            const int sh = rec.w;
             uint32_t y = m;
-            y &= y >> (sh & 63);
-            y &= y >> ((sh >> 6) & 63);
-            y &= y >> ((sh >> 12) & 63);
-            y &= y >> ((sh >> 18) & 63);
-            y &= y >> ((sh >> 24) & 63);
+            y &= y >> s0;
+            y &= y >> s1;
+            y &= y >> s2;
+            y &= y >> s3;
+            y &= y >> s4;
             if (y) {
               start = t0 + __ffs(y) - 1;
               break;
             }
           }
-          carry = zm ? __clz(zm) : carry + 32;
+          carry = z < 0 ? carry + 32 : __clz(~m);
           t0 += 32;
           if (t0 >= H) {  // cannot happen for valid instances
             start = H;
@@ -222,14 +242,16 @@ __device__ __forceinline__ int sgs_time_warp(const int4* __restrict__ info,
         }
       }
       const int fin = start + dur;
-      for (int t = hw + lane; t < start; t += 32) {
-        tau[t * W] = cap0;
-        if (W == 2) tau[t * W + 1] = cap1;
-      }
+      if (start > hw)
+        for (int t = hw + lane; t < start; t += 32) {
+          sts32(a_tau + 4 * W * t, cap0);
+          if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+        }
       for (int t = start + lane; t < fin; t += 32) {
+        const uint32_t adr = a_tau + 4 * W * t;
         const bool old = t < hw;
-        tau[t * W] = (old ? tau[t * W] : cap0) - r0;
-        if (W == 2) tau[t * W + 1] = (old ? tau[t * W + 1] : cap1) - r1;
+        sts32(adr, (old ? lds32(adr) : cap0) - r0);
+        if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
       }
       hw = max(hw, fin);
     }
@@ -237,8 +259,8 @@ __device__ __forceinline__ int sgs_time_warp(const int4* __restrict__ info,
     cmax = max(cmax, fin);
     const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
     for (int e = lane; e < ecnt; e += 32) {
-      const int s = push_dat[e0 + e];
-      if (es[s] < fin) es[s] = fin;
+      const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
+      if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
     }
     if (starts_out && lane == 0) starts_out[act] = start;
     __syncwarp();
