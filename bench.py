@@ -53,7 +53,9 @@ def parse():
     ap.add_argument("--iters", type=int, default=1000, help="I_total per instance")
     ap.add_argument("--epochs", type=int, default=4, help="elite-exchange epochs (N > 1)")
     ap.add_argument("--group", type=int, default=None, help="TIME lanes per schedule")
-    ap.add_argument("--threads", type=int, default=512)
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
+    ap.add_argument("--no-steal", action="store_true",
+                    help="fixed worker-to-instance mapping (no tail balancing)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -213,7 +215,8 @@ def main() -> None:
                                   workers=args.workers, seed=1000 * rank)
     cfg = SolveConfig(total_iters=p.total_iters, workers=p.workers, pool_size=p.pool_size,
                       tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
-                      phi_max=p.phi_max, seed=p.seed, group=args.group, threads=args.threads)
+                      phi_max=p.phi_max, seed=p.seed, group=args.group, threads=args.threads,
+                      steal=not args.no_steal)
     solver = BatchSolver(insts, modes, cfg)
     solver.upload()
     stream = torch.cuda.current_stream()

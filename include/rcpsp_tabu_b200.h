@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 1
+#define RCPSP_ABI_VERSION 2
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -76,7 +76,10 @@ typedef struct RcpspSolveArgs {
     /* shape maxima of the launch group (shared-memory sizing) */
     int64_t h_max, e_max, m_max, rmax_max, words;
     int64_t group;              /* TIME lanes per schedule: 32, 16 or 8   */
-    int64_t threads;            /* threads per CTA                        */
+    int64_t threads;            /* threads per CTA (0 = auto: 2 CTAs/SM)  */
+    int64_t steal;              /* 1 = a worker whose instance has spent its
+                                 * budget moves on to instances with budget
+                                 * left (balances the batch tail; B > 1) */
 } RcpspSolveArgs;
 
 int rcpsp_abi_version(void);

@@ -322,7 +322,7 @@ class BatchStats:
 
 def orchestrate_batch(instances: list[ProjectInstance], params: SearchParams,
                       modes: list[EvalMode] | None = None, rules=DEFAULT_RULES,
-                      group: int | None = None, threads: int = 512) -> BatchStats:
+                      group: int | None = None, threads: int = 0) -> BatchStats:
     """Solve many instances at once: each gets its own working set and
     `params.workers` CTAs; all run concurrently on the GPU.  Modes default
     to the static rules per instance (BASELINE config: heuristic selection)."""

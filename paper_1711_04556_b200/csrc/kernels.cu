@@ -25,7 +25,8 @@ namespace {
 
 enum WsField {
   WS_CURSOR = 0, WS_TOTAL = 1, WS_PLANNED = 2, WS_CONSUMED = 3, WS_STOP = 4, WS_BEST = 5,
-  WS_BEST_MODE = 6, WS_FLOOR = 7, WS_POOL_EVALS = 8, WS_T0 = 9, WS_T1 = 10
+  WS_BEST_MODE = 6, WS_FLOOR = 7, WS_POOL_EVALS = 8, WS_T0 = 9, WS_T1 = 10, WS_ITERS = 11,
+  WS_EVALS = 12, WS_EXCH = 13, WS_DIV = 14, WS_FORCED = 15
 };
 enum WkField {
   WK_ITERS = 0, WK_EVALS = 1, WK_EXCH = 2, WK_DIV = 3, WK_FORCED = 4, WK_CHUNKS = 5,
@@ -88,9 +89,9 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
                             W == 2 ? I.capw[1] : 0u, I.hi, n, I.H, sa(tau), sa(es), sa(ord),
                             starts ? starts + static_cast<size_t>(b) * n : nullptr, err);
     } else {
-      cm = sgs_time_group<G, W>(I, tau, es, [&](int p) { return ord[p]; },
-                                reverse ? I.info_r : I.info_f, pd,
-                                starts ? starts + static_cast<size_t>(b) * n : nullptr, active,
+      cm = sgs_time_split<G, W>(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.req), I.capw[0],
+                                W == 2 ? I.capw[1] : 0u, I.hi, n, I.H, sa(tau), sa(es), sa(ord),
+                                active, starts ? starts + static_cast<size_t>(b) * n : nullptr,
                                 err);
     }
     if (active && lane_g == 0) cmax[b] = cm;
@@ -428,37 +429,48 @@ __device__ __forceinline__ int64_t ldcg64(const int64_t* p) {
   return static_cast<int64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
 }
 
+__device__ __forceinline__ void add64(int64_t* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// One CTA = one search worker.  Worker loop (search.run_worker): exchange
+// with its instance's working set under the instance lock (cooperation.py:
+// 276-329) -> optional diversify (search.py:77-94) -> evaluate the adopted
+// order (search.py:134-142) -> run_chunk (kernels.py:316-385).  With
+// A.steal, a worker whose instance has no budget left (or hit the critical
+// path) moves on to the next instance of the launch that still has budget,
+// so the batch finishes together; without it (the reference's fixed
+// worker-to-pool mapping, and exact B = 1 trajectories) it exits.
 template <int MODE, int G, int W>
 __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
-                                               SmemPlan plan) {
+                                                  int n_ids, SmemPlan plan) {
   int* smem = dsm;
   const int B = static_cast<int>(A.workers);
-  const int slot = blockIdx.x / B, wk = blockIdx.x % B;
-  const int iid = ids[slot];
+  const int slot0 = blockIdx.x / B, wk = blockIdx.x % B;
+  int slot = slot0;
+  int iid = ids[slot];
   const int tid = threadIdx.x;
   const int F = static_cast<int>(A.pool_size), T = static_cast<int>(A.tabu_size);
   CtaCtx c;
   cta_setup(c, A.blob + A.blob_off[iid], smem, plan, static_cast<int>(A.delta), T,
             A.moves_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max,
             A.cmax_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max, A.err);
-  const int n = c.I.n;
-  const size_t wid = static_cast<size_t>(iid) * B + wk;
+  const size_t wid = static_cast<size_t>(iid) * B + wk;  // this worker's rng / stats slot
   int64_t* st = A.w_stats + wid * 16;
-  int64_t* Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
   int* wtrace = A.collect_trace ? A.w_trace + wid * A.trace_cap : nullptr;
   int* wchunks = A.collect_trace ? A.w_chunks + wid * A.chunk_cap : nullptr;
+  const bool steal = A.steal != 0 && !A.collect_trace;
   Pcg64 rng;
-  long long s_iters = 0, s_evals = 0, s_exch = 0, s_div = 0, s_forced = 0;
   long long chunks = st[WK_CHUNKS], tlen = st[WK_TRACE];
   if (tid == 0) {
     rng.load(A.w_rng + wid * 6);
-    const unsigned long long t0 = globaltimer();
-    if (st[WK_T0] == 0) st[WK_T0] = static_cast<long long>(t0);
-    atomicMin(reinterpret_cast<unsigned long long*>(&Hd[WS_T0]), t0);
+    if (st[WK_T0] == 0) st[WK_T0] = static_cast<long long>(globaltimer());
   }
+  int64_t* Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
+  if (tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(&Hd[WS_T0]), globaltimer());
   int entry = -1, improved = 0, local_best = 0;
   long long granted = 0, used = 0;
-  const int floor_cmax = c.I.cpm;
+  int hops = 0;
   for (;;) {
     // ---------------- exchange (cooperation.py:276-329), under the lock
     if (tid == 0) {
@@ -471,12 +483,12 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
       const long long gbest = ldcg64(&Hd[WS_BEST]);
       if (improved) {
         int* dst = A.ent_order + eo * A.n_max;
-        for (int p = tid; p < n; p += blockDim.x) dst[p] = c.best[p];
+        for (int p = tid; p < c.I.n; p += blockDim.x) dst[p] = c.best[p];
         uint32_t* tl = A.ent_tabu + eo * T;
         for (int i = tid; i < T; i += blockDim.x) tl[i] = c.tabu_list[i];
         if (local_best < gbest) {
           int* bo = A.ws_best_order + static_cast<size_t>(iid) * A.n_max;
-          for (int p = tid; p < n; p += blockDim.x) bo[p] = c.best[p];
+          for (int p = tid; p < c.I.n; p += blockDim.x) bo[p] = c.best[p];
         }
       }
       __syncthreads();
@@ -533,8 +545,32 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
     if (c.scal[SC_NONE]) {
       __threadfence();
       __syncthreads();
-      if (tid == 0) atomicExch(&A.ws_lock[iid], 0);
-      break;
+      if (tid == 0) {
+        atomicExch(&A.ws_lock[iid], 0);
+        atomicMax(reinterpret_cast<unsigned long long*>(&Hd[WS_T1]), globaltimer());
+      }
+      if (!steal) break;
+      // ---------------- move on to an instance that still has budget
+      if (tid == 0) {
+        int next = -1;
+        for (int k = 1; k <= n_ids && next < 0; ++k) {
+          const int s2 = (slot + k) % n_ids;
+          const int64_t* H2 = A.ws_hdr + static_cast<size_t>(ids[s2]) * 16;
+          if (!ldcg64(&H2[WS_STOP]) && ldcg64(&H2[WS_PLANNED]) < A.epoch_limit) next = s2;
+        }
+        c.scal[SC_FLAG] = next;
+      }
+      __syncthreads();
+      const int next = c.scal[SC_FLAG];
+      if (next < 0 || ++hops > 4 * n_ids) break;
+      slot = next;
+      iid = ids[slot];
+      Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
+      __syncthreads();
+      stage_instance(A.blob + A.blob_off[iid], smem + plan.inst, c.I);
+      __syncthreads();
+      cta_init_rows(c);
+      continue;
     }
     entry = c.scal[SC_ENTRY];
     granted = c.scal[SC_GRANT];
@@ -544,7 +580,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
     {
       const size_t eo = static_cast<size_t>(iid) * F + entry;
       const int* src = A.ent_order + eo * A.n_max;
-      for (int p = tid; p < n; p += blockDim.x) c.base[p] = __ldcg(&src[p]);
+      for (int p = tid; p < c.I.n; p += blockDim.x) c.base[p] = __ldcg(&src[p]);
       const uint32_t* tl = A.ent_tabu + eo * T;
       for (int i = tid; i < T; i += blockDim.x) c.tabu_list[i] = __ldcg(&tl[i]);
     }
@@ -553,25 +589,30 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
     if (tid == 0) atomicExch(&A.ws_lock[iid], 0);
     cta_tabu_rebuild(c);
     // ---------------- run_worker body (search.py:189-194)
-    if (needs_div) {
-      cta_diversify(c, c.base, static_cast<int>(A.phi_steps), rng);
-      ++s_div;
-    }
-    ++s_exch;
+    if (needs_div) cta_diversify(c, c.base, static_cast<int>(A.phi_steps), rng);
     // ---------------- Worker.run_adopted (search.py:144-173)
     const int start_cmax = cta_eval_one<MODE, G, W>(c, c.base);
-    ++s_evals;
-    for (int p = tid; p < n; p += blockDim.x) c.best[p] = c.base[p];
+    for (int p = tid; p < c.I.n; p += blockDim.x) c.best[p] = c.base[p];
     __syncthreads();
     ChunkOut o = run_chunk_cta<MODE, G, W>(c, static_cast<int>(granted), adopted, start_cmax,
-                                           best_known, floor_cmax,
+                                           best_known, c.I.cpm,
                                            wtrace ? wtrace + tlen : nullptr);
     used = o.iters;
     improved = o.improved;
     local_best = o.local_best;
-    s_iters += o.iters;
-    s_evals += o.evals;
-    s_forced += o.forced;
+    if (tid == 0) {
+      // per-instance counters (RunStats) and per-worker ones (WorkerStats)
+      add64(&Hd[WS_ITERS], o.iters);
+      add64(&Hd[WS_EVALS], o.evals + 1);
+      add64(&Hd[WS_EXCH], 1);
+      add64(&Hd[WS_DIV], needs_div ? 1 : 0);
+      add64(&Hd[WS_FORCED], o.forced);
+      st[WK_ITERS] += o.iters;
+      st[WK_EVALS] += o.evals + 1;
+      st[WK_EXCH] += 1;
+      st[WK_DIV] += needs_div ? 1 : 0;
+      st[WK_FORCED] += o.forced;
+    }
     if (wtrace) {
       if (tid == 0 && chunks < A.chunk_cap) wchunks[chunks] = o.iters;
       ++chunks;
@@ -579,16 +620,9 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
     }
   }
   if (tid == 0) {
-    st[WK_ITERS] += s_iters;
-    st[WK_EVALS] += s_evals;
-    st[WK_EXCH] += s_exch;
-    st[WK_DIV] += s_div;
-    st[WK_FORCED] += s_forced;
     st[WK_CHUNKS] = chunks;
     st[WK_TRACE] = tlen;
-    const unsigned long long t1 = globaltimer();
-    st[WK_T1] = static_cast<long long>(t1);
-    atomicMax(reinterpret_cast<unsigned long long*>(&Hd[WS_T1]), t1);
+    st[WK_T1] = static_cast<long long>(globaltimer());
     rng.store(A.w_rng + wid * 6);
   }
 }
@@ -677,17 +711,42 @@ size_t smem_optin() {
   return static_cast<size_t>(optin);
 }
 
-// search-kernel plan: most warps (<= want) and CAP lanes whose smem fits
-bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
-                     int T, int want_threads, SmemPlan& p, int& threads) {
-  const size_t limit = smem_optin();
-  for (threads = want_threads; threads >= 32; threads -= 32) {
+size_t smem_per_sm() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  }
+  return static_cast<size_t>(v);
+}
+
+// search-kernel plan: the most warps (<= want) and CAP lanes whose shared
+// memory fits `limit` bytes
+bool fit_plan_limit(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
+                    int T, int want_threads, size_t limit, int min_threads, SmemPlan& p,
+                    int& threads) {
+  for (threads = want_threads; threads >= min_threads; threads -= 32) {
     for (int lanes = 32; lanes >= (mode == MODE_CAPACITY ? 1 : 32); --lanes) {
       p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes);
       if (static_cast<size_t>(p.total) * 4 <= limit) return true;
     }
   }
   return false;
+}
+
+// want_threads == 0: prefer two resident CTAs per SM (>= 256 threads each),
+// else one CTA with as many warps as fit
+bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
+                     int T, int want_threads, SmemPlan& p, int& threads) {
+  if (want_threads == 0) {
+    const size_t half = smem_per_sm() / 2 - 1024;
+    if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, 512, half, 256, p, threads))
+      return true;
+    want_threads = 512;
+  }
+  return fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, want_threads, smem_optin(), 32, p,
+                        threads);
 }
 
 template <class Kern>
@@ -844,7 +903,7 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   if (n_ids <= 0) return 0;
   RcpspSolveArgs A = *args;
   const int threads = static_cast<int>(A.threads);
-  if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
+  if (threads % 32 || threads < 0 || threads > 512) return fail("threads must be 0 (auto) or 32..512, x32");
   if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words),
@@ -859,7 +918,7 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
     const int grid = n_ids * static_cast<int>(A.workers);
-    k<<<grid, nt, p.total * 4, s>>>(A, inst_ids, p);
+    k<<<grid, nt, p.total * 4, s>>>(A, inst_ids, n_ids, p);
     return launch_check("k_solve");
   });
 }

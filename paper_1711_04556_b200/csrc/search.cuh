@@ -268,37 +268,37 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req
   }
 }
 
-// TIME, G < 32 lanes per schedule
+// TIME, G = 16 / 8 lanes per schedule (S = 32/G schedules per warp)
 template <int G, int W>
-__device__ __noinline__ void eval_moves_timeg(const SInst& I, int o_base, int o_evs,
+__device__ __noinline__ void eval_moves_split(int o_info, int o_sdat, int o_req, int o_base,
+                                              int o_evs, uint32_t cap0, uint32_t cap1,
+                                              uint32_t hi, int n, int H,
                                               const uint32_t* __restrict__ moves,
                                               int* __restrict__ cmax_out, int n_feas,
                                               int warp_words, int* err) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   constexpr int S = 32 / G;
-  const int grp = lane / G;
-  const int gid = warp * S + grp;
-  const int ngroups = nw * S;
-  const int gwords = (I.H + 1) * W + I.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int grp = lane / G, lg = lane & (G - 1);
+  const int gwords = (H + 1) * W + 2 * n;
   const int* base = dsm + o_base;
-  uint32_t* tau = reinterpret_cast<uint32_t*>(dsm + o_evs + warp * warp_words + grp * gwords);
-  int* es = reinterpret_cast<int*>(tau) + (I.H + 1) * W;
-  for (int b = 0; b < n_feas; b += ngroups) {
-    const int idx = b + gid;
+  int* tau = dsm + o_evs + warp * warp_words + grp * gwords;
+  int* es = tau + (H + 1) * W;
+  int* ord = es + n;
+  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_sdat), a_req = sa(dsm + o_req),
+                 a_tau = sa(tau), a_es = sa(es), a_ord = sa(ord);
+  for (int b = 0; b < n_feas; b += nw * S) {
+    const int idx = b + warp * S + grp;
     const bool active = idx < n_feas;
     if (!__any_sync(FULL_MASK, active)) break;
-    int u = -1, v = -1, au = 0, av = 0;
     if (active) {
       const uint32_t mv = moves[idx];
-      u = static_cast<int>(mv >> 16);
-      v = static_cast<int>(mv & 0xffff);
-      au = base[v];
-      av = base[u];
+      const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+      for (int p = lg; p < n; p += G) ord[p] = base[p == u ? v : (p == v ? u : p)];
     }
-    const int cm = sgs_time_group<G, W>(
-        I, tau, es, [&](int p) { return p == u ? au : (p == v ? av : base[p]); }, I.info_f,
-        I.sdat, nullptr, active, err);
-    if (active && (lane & (G - 1)) == 0) cmax_out[idx] = cm;
+    __syncwarp();
+    const int cm = sgs_time_split<G, W>(a_info, a_push, a_req, cap0, cap1, hi, n, H, a_tau, a_es,
+                                        a_ord, active, nullptr, err);
+    if (active && lg == 0) cmax_out[idx] = cm;
   }
 }
 
@@ -330,8 +330,9 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
                            soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
                            c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
     } else {
-      eval_moves_timeg<G, W>(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
-                             c.warp_words, c.err);
+      eval_moves_split<G, W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
+                             soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
+                             c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
     }
   } else {
     eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
@@ -483,7 +484,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + n) + n;
+  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + 2 * n);
   return cap_lanes * cap_thread_words(n, m, rmax);
 }
 

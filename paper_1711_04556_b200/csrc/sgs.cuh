@@ -32,131 +32,6 @@ __device__ __forceinline__ bool fits1(uint32_t w, uint32_t r, uint32_t hi) {
   return (((w | hi) - r) & hi) == hi;
 }
 
-// Time-indexed SGS for one schedule per G-lane group.
-//   tau:   the group's profile, (H+1)*W words, slot t at tau[t*W + w]
-//   es:    the group's [n] earliest-start scratch
-//   act_at(pos) -> activity at position pos (group-uniform)
-//   info / push_dat: per-activity records (common.cuh) and the edge targets
-//     finish times propagate to (I.info_f + I.sdat forward; I.info_r +
-//     I.pdat for the reversed project)
-//   starts_out: optional [n] (lane 0 of the group writes)
-// Returns the makespan (group-uniform).  `active` false: the group only
-// joins the warp-collective votes.
-//
-// Per activity: record + es in two LDS; no scan when the activity needs no
-// resource, or when es is at/after the materialised profile (everything there
-// is free).  Otherwise each round tests G slots (one LDS each lane), ballots,
-// and resolves the earliest window branch-free: the carried run from the
-// previous round, else the first run of `dur` ones inside the round (five
-// precomputed doubling shifts).
-template <int G, int W, class ActFn>
-__device__ __forceinline__ int sgs_time_group(const SInst& I, uint32_t* __restrict__ tau,
-                                              int* __restrict__ es, ActFn act_at,
-                                              const int4* __restrict__ info,
-                                              const int* __restrict__ push_dat,
-                                              int* __restrict__ starts_out, bool active,
-                                              int* err) {
-  const int lane = threadIdx.x & 31;
-  const int lane_g = lane & (G - 1);
-  const int gshift = lane & ~(G - 1) & 31;
-  constexpr uint32_t GM = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
-  const int n = I.n, H = I.H;
-  const uint32_t hi = I.hi;
-  const uint32_t cap0 = I.capw[0];
-  const uint32_t cap1 = W == 2 ? I.capw[1] : 0u;
-
-  if (active)
-    for (int a = lane_g; a < n; a += G) es[a] = 0;
-  __syncwarp();
-
-  int cmax = 0;
-  int hw = 0;  // profile slots [0, hw) are materialised; >= hw are at capacity
-  for (int pos = 0; pos < n; ++pos) {
-    int4 rec = make_int4(0, 0, 0, 0);
-    int act = 0, esv = 0;
-    uint32_t r1 = 0;
-    if (active) {
-      act = act_at(pos);
-      rec = info[act];
-      esv = es[act];
-      if (W == 2) r1 = I.req[act * 2 + 1];
-    }
-    const int dur = rec.x;
-    const uint32_t r0 = static_cast<uint32_t>(rec.y);
-    const bool need = dur > 0 && (r0 | r1) != 0;
-    int start = esv;
-    bool done = !(need && esv < hw);
-    int t0 = esv, carry = 0;
-    while (__any_sync(FULL_MASK, !done)) {
-      bool ok = false;
-      if (!done) {
-        const int t = t0 + lane_g;
-        uint32_t w0 = cap0, w1 = cap1;
-        if (t < hw) {
-          w0 = tau[t * W];
-          if (W == 2) w1 = tau[t * W + 1];
-        }
-        ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
-      }
-      const uint32_t m = (__ballot_sync(FULL_MASK, ok) >> gshift) & GM;
-      if (!done) {
-        const uint32_t zm = ~m & GM;
-        const int z = zm ? __ffs(zm) - 1 : G;
-        uint32_t y = 0;
-        if (dur <= G) {
-          const int sh = rec.w;
-          y = m;
-          y &= y >> (sh & 63);
-          y &= y >> ((sh >> 6) & 63);
-          y &= y >> ((sh >> 12) & 63);
-          y &= y >> ((sh >> 18) & 63);
-          y &= y >> ((sh >> 24) & 63);
-        }
-        if (carry + z >= dur) {
-          start = t0 - carry;
-          done = true;
-        } else if (y) {
-          start = t0 + __ffs(y) - 1;
-          done = true;
-        } else {
-          carry = zm ? __clz(~(m << (32 - G))) : carry + G;
-          t0 += G;
-          if (t0 >= H) {  // cannot happen for valid instances
-            start = H;
-            done = true;
-            if (lane_g == 0) set_err(err, DE_NO_WINDOW);
-          }
-        }
-      }
-    }
-    if (active) {
-      const int fin = start + dur;
-      if (need) {
-        // materialise [hw, start) at capacity, subtract the demand on [start, fin)
-        for (int t = hw + lane_g; t < start; t += G) {
-          tau[t * W] = cap0;
-          if (W == 2) tau[t * W + 1] = cap1;
-        }
-        for (int t = start + lane_g; t < fin; t += G) {
-          const bool old = t < hw;
-          tau[t * W] = (old ? tau[t * W] : cap0) - r0;
-          if (W == 2) tau[t * W + 1] = (old ? tau[t * W + 1] : cap1) - r1;
-        }
-        hw = max(hw, fin);
-      }
-      cmax = max(cmax, fin);
-      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-      for (int e = lane_g; e < ecnt; e += G) {
-        const int s = push_dat[e0 + e];
-        if (es[s] < fin) es[s] = fin;
-      }
-      if (starts_out && lane_g == 0) starts_out[act] = start;
-    }
-    __syncwarp();
-  }
-  return cmax;
-}
-
 // ---- explicit shared-memory access (32-bit shared addresses)
 __device__ __forceinline__ uint32_t sa(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -177,7 +52,7 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 }
 
 // Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same
-// results as sgs_time_group; every branch is warp-uniform and every shared
+// results as the reference's time-indexed SGS; every branch is warp-uniform and every shared
 // access goes through a precomputed 32-bit shared address.
 //   a_ord:  the warp's order [n] (already swapped)      a_info: records [n]
 //   a_push: edge targets of the push graph               a_req:  packed demand
@@ -263,6 +138,108 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
       if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
     }
     if (starts_out && lane == 0) starts_out[act] = start;
+    __syncwarp();
+  }
+  return cmax;
+}
+
+// Split-warp time-indexed SGS: S = 32/G schedules per warp (G = 16 or 8
+// lanes each), same results as sgs_time_warp.  Group state is predicated
+// instead of branched (the warp runs the scan rounds until every group has
+// found its window), so per-activity work -- record loads, update, push -- is
+// shared by S schedules in one instruction stream.
+//   a_ord/a_es/a_tau: this lane's group arrays (32-bit shared addresses)
+//   active: this group has a schedule (false: it only joins the votes)
+template <int G, int W>
+__device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, uint32_t a_req,
+                                              uint32_t cap0, uint32_t cap1, uint32_t hi, int n,
+                                              int H, uint32_t a_tau, uint32_t a_es,
+                                              uint32_t a_ord, bool active,
+                                              int* __restrict__ starts_out, int* err) {
+  static_assert(G == 16 || G == 8, "split evaluator is for 16 or 8 lanes per schedule");
+  constexpr uint32_t GM = (1u << G) - 1u;
+  const int lane = threadIdx.x & 31;
+  const int lg = lane & (G - 1);
+  const int gshift = lane & ~(G - 1);
+  if (active)
+    for (int a = lg; a < n; a += G) sts32(a_es + 4 * a, 0);
+  __syncwarp();
+  int cmax = 0, hw = 0;
+  for (int pos = 0; pos < n; ++pos) {
+    int4 rec = make_int4(0, 0, 0, 0);
+    int act = 0, esv = 0;
+    uint32_t r1 = 0;
+    if (active) {
+      act = static_cast<int>(lds32(a_ord + 4 * pos));
+      rec = lds128(a_info + 16 * act);
+      esv = static_cast<int>(lds32(a_es + 4 * act));
+      if (W == 2) r1 = lds32(a_req + 8 * act + 4);
+    }
+    const int dur = rec.x;
+    const uint32_t r0 = static_cast<uint32_t>(rec.y);
+    const bool need = dur > 0 && (r0 | r1) != 0;
+    bool scanning = need && esv < hw;
+    int start = esv;
+    if (__any_sync(FULL_MASK, scanning)) {
+      const int sh = rec.w;
+      const int s0 = sh & 63, s1 = (sh >> 6) & 63, s2 = (sh >> 12) & 63, s3 = (sh >> 18) & 63,
+                s4 = (sh >> 24) & 63;
+      int t0 = esv, carry = 0;
+      do {
+        const int t = t0 + lg;
+        uint32_t w0 = cap0, w1 = cap1;
+        if (scanning && t < hw) {
+          w0 = lds32(a_tau + 4 * W * t);
+          if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
+        }
+        const bool ok = scanning && t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
+        const uint32_t m = (__ballot_sync(FULL_MASK, ok) >> gshift) & GM;
+        const int z = __ffs(~m) - 1;  // first blocked slot, G when none
+        uint32_t y = m;
+        y &= y >> s0;
+        y &= y >> s1;
+        y &= y >> s2;
+        y &= y >> s3;
+        y &= y >> s4;
+        const bool fc = carry + z >= dur;
+        const int cand = fc ? t0 - carry : t0 + __ffs(y) - 1;
+        if (scanning && (fc || y != 0)) {
+          start = cand;
+          scanning = false;
+        } else if (scanning) {
+          carry = z == G ? carry + G : __clz(~(m << (32 - G)));
+          t0 += G;
+          if (t0 >= H) {  // cannot happen for valid instances
+            start = H;
+            scanning = false;
+            if (lg == 0) set_err(err, DE_NO_WINDOW);
+          }
+        }
+      } while (__any_sync(FULL_MASK, scanning));
+    }
+    if (active) {
+      const int fin = start + dur;
+      if (need) {
+        for (int t = hw + lg; t < start; t += G) {
+          sts32(a_tau + 4 * W * t, cap0);
+          if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+        }
+        for (int t = start + lg; t < fin; t += G) {
+          const uint32_t adr = a_tau + 4 * W * t;
+          const bool old = t < hw;
+          sts32(adr, (old ? lds32(adr) : cap0) - r0);
+          if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+        }
+        hw = max(hw, fin);
+      }
+      cmax = max(cmax, fin);
+      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+      for (int e = lg; e < ecnt; e += G) {
+        const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
+        if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+      }
+      if (starts_out && lg == 0) starts_out[act] = start;
+    }
     __syncwarp();
   }
   return cmax;

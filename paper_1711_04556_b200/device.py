@@ -32,7 +32,8 @@ HDR = 32
  B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT) = range(16, 27)
 
 WS_FIELDS = dict(cursor=0, total=1, planned=2, consumed=3, stop=4, best=5, best_mode=6, floor=7,
-                 pool_evals=8, t0=9, t1=10)
+                 pool_evals=8, t0=9, t1=10, iterations=11, evaluations=12, exchanges=13,
+                 diversifications=14, forced=15)
 WK_FIELDS = dict(iterations=0, evaluations=1, exchanges=2, diversifications=3, forced=4,
                  chunks=5, trace_len=6, t0=7, t1=8)
 
@@ -353,7 +354,8 @@ class SolveConfig:
     collect_trace: bool = False
     grant_cap: int = 0
     group: int | None = None
-    threads: int = 512
+    threads: int = 0          # 0 = auto (two CTAs per SM when they fit)
+    steal: bool = True        # B > 1: idle workers help instances with budget left
 
     @property
     def block_iters(self) -> int:
@@ -499,6 +501,7 @@ class BatchSolver:
         a.words = words
         a.group = cfg.group if cfg.group is not None else pick_group(self.n_max)
         a.threads = cfg.threads
+        a.steal = int(cfg.steal and cfg.workers > 1 and not cfg.collect_trace)
         return a
 
     def pool_init(self, stream=None) -> None:
@@ -536,7 +539,7 @@ class BatchSolver:
         ws = self.w_stats.cpu().numpy()
         I = len(self.instances)
         pool = hdr[:, WS_FIELDS["pool_evals"]]
-        evals = pool + ws[:, :, WK_FIELDS["evaluations"]].sum(1)
+        evals = pool + hdr[:, WS_FIELDS["evaluations"]]
         t0 = hdr[:, WS_FIELDS["t0"]].astype(np.float64)
         t1 = hdr[:, WS_FIELDS["t1"]].astype(np.float64)
         span = np.where(t1 > 0, (t1 - t0) * 1e-9, 0.0)
@@ -561,9 +564,9 @@ class BatchSolver:
             iterations=hdr[:, WS_FIELDS["consumed"]].astype(np.int64),
             evaluations=evals.astype(np.int64),
             pool_evaluations=pool.astype(np.int64),
-            exchanges=ws[:, :, WK_FIELDS["exchanges"]].sum(1),
-            diversifications=ws[:, :, WK_FIELDS["diversifications"]].sum(1),
-            forced=ws[:, :, WK_FIELDS["forced"]].sum(1),
+            exchanges=hdr[:, WS_FIELDS["exchanges"]].astype(np.int64),
+            diversifications=hdr[:, WS_FIELDS["diversifications"]].astype(np.int64),
+            forced=hdr[:, WS_FIELDS["forced"]].astype(np.int64),
             stopped=hdr[:, WS_FIELDS["stop"]].astype(bool),
             device_ms=device_ms, search_ms=search_ms, inst_wall_s=span, traces=traces,
             n_launches=self.launches)
