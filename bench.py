@@ -208,6 +208,7 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1711_04556_b200 import SearchParams, decide_static, extract_features, synth
     from paper_1711_04556_b200.device import (BatchSolver, SolveConfig, smem_bandwidth)
+    from paper_1711_04556_b200.population import EliteExchange, run_epochs
 
     insts = synth.benchmark_batch(args.config, args.instances)
     modes = [int(decide_static(extract_features(x))) for x in insts]
@@ -224,28 +225,22 @@ def main() -> None:
     epochs = args.epochs if ws > 1 else 1
     n_max = solver.n_max
     I = len(insts)
-    if ws > 1:
-        mine = torch.zeros((I, n_max), dtype=torch.int32, device="cuda")
-        mine_c = torch.zeros(I, dtype=torch.int32, device="cuda")
-        allo = torch.zeros((ws, I, n_max), dtype=torch.int32, device="cuda")
-        allc = torch.zeros((ws, I), dtype=torch.int32, device="cuda")
+    exchange = EliteExchange(solver, I, n_max) if ws > 1 else None
 
     def one_step(timed_search: list | None = None) -> None:
         solver.pool_init(stream)
-        for e in range(epochs):
-            limit = args.iters * (e + 1) // epochs
-            if timed_search is not None:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            solver.search(epoch_limit=limit, stream=stream)
-            if timed_search is not None:
-                b.record(stream)
-                timed_search.append((a, b))
-            if ws > 1 and e + 1 < epochs:
-                solver.export_elites(mine, mine_c, stream)
-                dist.all_gather_into_tensor(allo, mine)
-                dist.all_gather_into_tensor(allc, mine_c)
-                solver.merge_elites(allo, allc, ws, stream)
+        marks: list = []
+
+        def mark(begin: bool) -> None:
+            if timed_search is None:
+                return
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            marks.append(ev)
+            if not begin:
+                timed_search.append((marks[-2], marks[-1]))
+
+        run_epochs(solver, args.iters, epochs, exchange, stream, on_search=mark)
 
     for _ in range(args.warmup):
         solver.reset()
@@ -333,10 +328,14 @@ def main() -> None:
     if pk.exists():
         peaks = json.loads(pk.read_text())
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic of the dominant kernel: ncu bytes per evaluated schedule
+    # (profiles/ncu_traffic.json) x the schedules one timed k_solve launch evaluated
     traffic = None
     tr = ROOT / "profiles" / "ncu_traffic.json"
     if tr.exists():
-        traffic = json.loads(tr.read_text()).get(args.config)
+        rec = json.loads(tr.read_text()).get(args.config)
+        if rec:
+            traffic = rec["dram_bytes_per_schedule"] * search_evals / (args.steps * epochs)
 
     line = {
         "metric": METRIC, "value": value, "unit": "schedules/s", "n_gpus": ws,

@@ -268,3 +268,44 @@ def test_multi_worker_solve(ginst):
         assert st.best_cmax >= critical_path_length(inst)
         assert st.feasible and st.exchanges >= workers
         assert st.evaluations > 400
+
+
+def test_merge_elites_model(ginst):
+    """k_export_elites / k_merge_elites follow the host model in test_multigpu.py."""
+    import torch
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    from test_multigpu import merge_model
+    insts = [ginst["genr30s0"], ginst["genr30s1"]]
+    cfg = SolveConfig(total_iters=10, workers=1, pool_size=6, tabu_size=60, delta=30,
+                      phi_steps=20, phi_max=3, seed=3)
+    s = BatchSolver(insts, [1, 1], cfg)
+    s.upload()
+    s.pool_init()
+    torch.cuda.synchronize()
+    I, n_max = 2, s.n_max
+    mine = torch.zeros((I, n_max), dtype=torch.int32, device="cuda")
+    mine_c = torch.zeros(I, dtype=torch.int32, device="cuda")
+    s.export_elites(mine, mine_c)
+    pool_c = s.ent_cmax.cpu().numpy().copy()
+    pool_o = s.ent_order.cpu().numpy().copy()
+    best = s.ws_hdr.cpu().numpy()[:, 5].copy()
+    best_o = s.best_order.cpu().numpy().copy()
+    assert mine_c.cpu().numpy().tolist() == best.tolist()
+    assert (mine.cpu().numpy() == best_o).all()
+    # two foreign sources: one better than everything, one duplicate makespan
+    rng = np.random.default_rng(0)
+    src_c = np.stack([best - 3, pool_c[:, 1]]).astype(np.int32)          # [src, inst]
+    src_o = np.stack([[rng.permutation(n_max) for _ in range(I)] for _ in range(2)]).astype(np.int32)
+    s.merge_elites(torch.from_numpy(src_o.reshape(2 * I, n_max)).cuda(),
+                   torch.from_numpy(src_c.reshape(-1)).cuda(), 2)
+    got_c = s.ent_cmax.cpu().numpy()
+    got_o = s.ent_order.cpu().numpy()
+    got_b = s.ws_hdr.cpu().numpy()[:, 5]
+    for i in range(I):
+        n = insts[i].n_activities
+        pc, po, b, bo = merge_model(pool_c[i], pool_o[i, :, :n], int(best[i]), best_o[i, :n],
+                                    src_o[:, i, :n], src_c[:, i])
+        assert got_c[i].tolist() == pc
+        assert got_o[i, :, :n].tolist() == po
+        assert int(got_b[i]) == b
+        assert s.best_order.cpu().numpy()[i, :n].tolist() == bo
