@@ -39,10 +39,11 @@ __device__ __forceinline__ void set_err(int* err, int code) {
 // Shared-memory view of one instance.  All arrays are int32 / uint32.
 // Per-activity record of the TIME evaluator (one LDS.128 per activity):
 //   x = duration, y = packed demand word 0,
-//   z = push span: first edge | (edge count << 16) of the graph finish times
-//       propagate along (successors forward, predecessors for the reversed
-//       project), w = the doubling shifts of the run-of-`dur` window test
-//       (5 fields of 6 bits, see window_shifts).
+//   z = push span: first edge | (edge count << 16) of the activities whose
+//       earliest start this one's finish time bounds (successors forward,
+//       predecessors for the reversed project),
+//   w = the doubling shifts of the run-of-`dur` window test (5 fields of 5
+//       bits, consumed by wrap-mode funnel shifts; see window_shifts).
 struct SInst {
   int n, m, H, e, W, rmax, cpm;
   uint32_t hi;           // high bit of every packed resource lane (TIME fits test)
@@ -65,11 +66,14 @@ __host__ __device__ __forceinline__ int inst_smem_words(int n, int m, int e, int
 
 // y &= y >> s_i (i = 1..5) turns a slot mask into "a run of d ones starts
 // here" (d <= 32): s_i = min(acc, d - acc), acc += s_i, acc starting at 1.
+// Fields are 5 bits wide at bit 5*i (every s_i <= 16); a wrap-mode funnel
+// shift uses only the low 5 bits of its amount, so field i is applied as
+// shf.r.wrap(y, 0, packed >> 5*i) without masking.
 __host__ __device__ __forceinline__ int window_shifts(int d) {
   int packed = 0, acc = 1;
   for (int i = 0; i < 5; ++i) {
     const int s = d > acc ? (acc < d - acc ? acc : d - acc) : 0;
-    packed |= s << (6 * i);
+    packed |= s << (5 * i);
     acc += s;
   }
   return packed;

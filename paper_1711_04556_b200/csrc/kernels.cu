@@ -85,11 +85,11 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
     int cm;
     if constexpr (G == 32) {
       if (!active) return;
-      cm = sgs_time_warp<W>(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.req), I.capw[0],
+      cm = sgs_time_warp<W>(sa(reverse ? I.info_r : I.info_f), sa(reverse ? I.pdat : I.sdat), sa(I.req), I.capw[0],
                             W == 2 ? I.capw[1] : 0u, I.hi, n, I.H, sa(tau), sa(es), sa(ord),
                             starts ? starts + static_cast<size_t>(b) * n : nullptr, err);
     } else {
-      cm = sgs_time_split<G, W>(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.req), I.capw[0],
+      cm = sgs_time_split<G, W>(sa(reverse ? I.info_r : I.info_f), sa(reverse ? I.pdat : I.sdat), sa(I.req), I.capw[0],
                                 W == 2 ? I.capw[1] : 0u, I.hi, n, I.H, sa(tau), sa(es), sa(ord),
                                 active, starts ? starts + static_cast<size_t>(b) * n : nullptr,
                                 err);
@@ -265,7 +265,7 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
   const int* pd = reverse ? I.pdat : I.sdat;
   int cm;
   if constexpr (MODE == MODE_TIME) {
-    cm = sgs_time_warp<W>(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.req), I.capw[0],
+    cm = sgs_time_warp<W>(sa(reverse ? I.info_r : I.info_f), sa(reverse ? I.pdat : I.sdat), sa(I.req), I.capw[0],
                           W == 2 ? I.capw[1] : 0u, I.hi, I.n, I.H, sa(scr),
                           sa(scr + (I.H + 1) * W), sa(ord), starts, err);
   } else {

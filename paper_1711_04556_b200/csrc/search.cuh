@@ -241,7 +241,7 @@ __device__ __forceinline__ int soff(const void* p) {
 
 // TIME, one warp per schedule
 template <int W>
-__device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req, int o_base,
+__device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req, int o_base,
                                                int o_evs, uint32_t cap0, uint32_t cap1,
                                                uint32_t hi, int n, int H,
                                                const uint32_t* __restrict__ moves,
@@ -249,13 +249,13 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req
                                                int warp_words, int* err) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int4* info = reinterpret_cast<const int4*>(dsm + o_info);
-  const int* sdat = dsm + o_sdat;
+  const int* pull = dsm + o_pull;
   const uint32_t* req = reinterpret_cast<const uint32_t*>(dsm + o_req);
   const int* base = dsm + o_base;
   uint32_t* tau = reinterpret_cast<uint32_t*>(dsm + o_evs + warp * warp_words);
   int* es = dsm + o_evs + warp * warp_words + (H + 1) * W;
   int* ord = es + n;
-  const uint32_t a_info = sa(info), a_push = sa(sdat), a_req = sa(req), a_tau = sa(tau),
+  const uint32_t a_info = sa(info), a_push = sa(pull), a_req = sa(req), a_tau = sa(tau),
                  a_es = sa(es), a_ord = sa(ord);
   for (int idx = warp; idx < n_feas; idx += nw) {
     const uint32_t mv = moves[idx];
@@ -270,7 +270,7 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_sdat, int o_req
 
 // TIME, G = 16 / 8 lanes per schedule (S = 32/G schedules per warp)
 template <int G, int W>
-__device__ __noinline__ void eval_moves_split(int o_info, int o_sdat, int o_req, int o_base,
+__device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req, int o_base,
                                               int o_evs, uint32_t cap0, uint32_t cap1,
                                               uint32_t hi, int n, int H,
                                               const uint32_t* __restrict__ moves,
@@ -284,7 +284,7 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_sdat, int o_req,
   int* tau = dsm + o_evs + warp * warp_words + grp * gwords;
   int* es = tau + (H + 1) * W;
   int* ord = es + n;
-  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_sdat), a_req = sa(dsm + o_req),
+  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_tau = sa(tau), a_es = sa(es), a_ord = sa(ord);
   for (int b = 0; b < n_feas; b += nw * S) {
     const int idx = b + warp * S + grp;

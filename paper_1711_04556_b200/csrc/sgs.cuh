@@ -51,9 +51,28 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// wrap-mode funnel shift: y >> (s & 31) (the window shift fields are 5 bits)
+__device__ __forceinline__ uint32_t shr_wrap(uint32_t y, int s) {
+  return __funnelshift_r(y, 0u, static_cast<uint32_t>(s));
+}
+
+// run of `dur` ones: y &= y >> s_i for the five packed fields of `sh`
+__device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
+  uint32_t y = m;
+  y &= shr_wrap(y, sh);
+  y &= shr_wrap(y, sh >> 5);
+  y &= shr_wrap(y, sh >> 10);
+  y &= shr_wrap(y, sh >> 15);
+  y &= shr_wrap(y, sh >> 20);
+  return y;
+}
+
 // Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same
-// results as the reference's time-indexed SGS; every branch is warp-uniform and every shared
-// access goes through a precomputed 32-bit shared address.
+// results as the reference's time-indexed SGS; every branch is warp-uniform
+// and every shared access goes through a precomputed 32-bit shared address.
+// The next activity's order entry and record depend only on the order, so
+// they are loaded one activity ahead; precedence is pushed (finish time ->
+// successors' es) so an activity's es is a single load.
 //   a_ord:  the warp's order [n] (already swapped)      a_info: records [n]
 //   a_push: edge targets of the push graph               a_req:  packed demand
 //   a_tau:  profile (H+1)*W words                        a_es:   [n] scratch
@@ -67,10 +86,12 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
   for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
   int cmax = 0, hw = 0;
+  int act = static_cast<int>(lds32(a_ord));
+  int4 rec = lds128(a_info + 16 * act);
   for (int pos = 0; pos < n; ++pos) {
-    const int act = static_cast<int>(lds32(a_ord + 4 * pos));
-    const int4 rec = lds128(a_info + 16 * act);
     const int esv = static_cast<int>(lds32(a_es + 4 * act));
+    const int act_n = static_cast<int>(lds32(a_ord + 4 * min(pos + 1, n - 1)));
+    const int4 rec_n = lds128(a_info + 16 * act_n);
     const int dur = rec.x;
     const uint32_t r0 = static_cast<uint32_t>(rec.y);
     const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
@@ -78,8 +99,6 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
     if (dur > 0 && (r0 | r1) != 0) {
       if (esv < hw) {
         const int sh = rec.w;
-        const int s0 = sh & 63, s1 = (sh >> 6) & 63, s2 = (sh >> 12) & 63,
-                  s3 = (sh >> 18) & 63, s4 = (sh >> 24) & 63;
         int t0 = esv, carry = 0;
         for (;;) {
           const int t = t0 + lane;
@@ -96,12 +115,7 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
             break;
           }
           if (dur <= 32) {
-            uint32_t y = m;
-            y &= y >> s0;
-            y &= y >> s1;
-            y &= y >> s2;
-            y &= y >> s3;
-            y &= y >> s4;
+            const uint32_t y = window_runs(m, sh);
             if (y) {
               start = t0 + __ffs(y) - 1;
               break;
@@ -138,6 +152,8 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
       if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
     }
     if (starts_out && lane == 0) starts_out[act] = start;
+    act = act_n;
+    rec = rec_n;
     __syncwarp();
   }
   return cmax;
@@ -165,14 +181,20 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
     for (int a = lg; a < n; a += G) sts32(a_es + 4 * a, 0);
   __syncwarp();
   int cmax = 0, hw = 0;
+  int act = 0;
+  int4 rec = make_int4(0, 0, 0, 0);
+  if (active) {
+    act = static_cast<int>(lds32(a_ord));
+    rec = lds128(a_info + 16 * act);
+  }
   for (int pos = 0; pos < n; ++pos) {
-    int4 rec = make_int4(0, 0, 0, 0);
-    int act = 0, esv = 0;
+    int esv = 0, act_n = 0;
+    int4 rec_n = make_int4(0, 0, 0, 0);
     uint32_t r1 = 0;
     if (active) {
-      act = static_cast<int>(lds32(a_ord + 4 * pos));
-      rec = lds128(a_info + 16 * act);
       esv = static_cast<int>(lds32(a_es + 4 * act));
+      act_n = static_cast<int>(lds32(a_ord + 4 * min(pos + 1, n - 1)));
+      rec_n = lds128(a_info + 16 * act_n);
       if (W == 2) r1 = lds32(a_req + 8 * act + 4);
     }
     const int dur = rec.x;
@@ -182,8 +204,6 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
     int start = esv;
     if (__any_sync(FULL_MASK, scanning)) {
       const int sh = rec.w;
-      const int s0 = sh & 63, s1 = (sh >> 6) & 63, s2 = (sh >> 12) & 63, s3 = (sh >> 18) & 63,
-                s4 = (sh >> 24) & 63;
       int t0 = esv, carry = 0;
       do {
         const int t = t0 + lg;
@@ -195,12 +215,7 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
         const bool ok = scanning && t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
         const uint32_t m = (__ballot_sync(FULL_MASK, ok) >> gshift) & GM;
         const int z = __ffs(~m) - 1;  // first blocked slot, G when none
-        uint32_t y = m;
-        y &= y >> s0;
-        y &= y >> s1;
-        y &= y >> s2;
-        y &= y >> s3;
-        y &= y >> s4;
+        const uint32_t y = window_runs(m, sh);
         const bool fc = carry + z >= dur;
         const int cand = fc ? t0 - carry : t0 + __ffs(y) - 1;
         if (scanning && (fc || y != 0)) {
@@ -240,6 +255,8 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
       }
       if (starts_out && lg == 0) starts_out[act] = start;
     }
+    act = act_n;
+    rec = rec_n;
     __syncwarp();
   }
   return cmax;
