@@ -67,11 +67,99 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
   return y;
 }
 
+// One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
+template <int W>
+__device__ __forceinline__ void time_step_warp(int act, const int4& rec, uint32_t a_push,
+                                               uint32_t a_req, uint32_t cap0, uint32_t cap1,
+                                               uint32_t hi, int H, uint32_t a_tau,
+                                               uint32_t a_es, int& hw, int& cmax,
+                                               int* __restrict__ starts_out, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int esv = static_cast<int>(lds32(a_es + 4 * act));
+  const int dur = rec.x;
+  const uint32_t r0 = static_cast<uint32_t>(rec.y);
+  const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
+  int start = esv;
+  if (dur > 0 && (r0 | r1) != 0) {
+    if (esv < hw) {
+      const int sh = rec.w;
+      int t0 = esv, carry = 0;
+      for (;;) {
+        const int t = t0 + lane;
+        uint32_t w0 = cap0, w1 = cap1;
+        if (t < hw) {
+          w0 = lds32(a_tau + 4 * W * t);
+          if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
+        }
+        const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
+        const uint32_t m = __ballot_sync(FULL_MASK, ok);
+        const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
+        if (carry + tz >= dur) {
+          start = t0 - carry;
+          break;
+        }
+        if (dur <= 32) {
+          const uint32_t y = window_runs(m, sh);
+          if (y) {
+            start = t0 + __ffs(y) - 1;
+            break;
+          }
+        }
+        carry = tz == 32 ? carry + 32 : __clz(~m);
+        t0 += 32;
+        if (t0 >= H) {  // cannot happen for valid instances
+          start = H;
+          if (lane == 0) set_err(err, DE_NO_WINDOW);
+          break;
+        }
+      }
+    }
+    const int fin = start + dur;
+    if (start > hw)
+      for (int t = hw + lane; t < start; t += 32) {
+        sts32(a_tau + 4 * W * t, cap0);
+        if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+      }
+    {  // subtract the demand on [start, fin): one slot per lane
+      const int t = start + lane;
+      if (lane < dur) {
+        const uint32_t adr = a_tau + 4 * W * t;
+        const bool old = t < hw;
+        sts32(adr, (old ? lds32(adr) : cap0) - r0);
+        if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+      }
+      if (dur > 32)
+        for (int tt = t + 32; tt < fin; tt += 32) {
+          const uint32_t adr = a_tau + 4 * W * tt;
+          const bool old = tt < hw;
+          sts32(adr, (old ? lds32(adr) : cap0) - r0);
+          if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+        }
+    }
+    hw = max(hw, fin);
+  }
+  const int fin = start + dur;
+  cmax = max(cmax, fin);
+  const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+  if (lane < ecnt) {  // push the finish time to the successors' es
+    const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + lane));
+    if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+  }
+  if (ecnt > 32)
+    for (int e = lane + 32; e < ecnt; e += 32) {
+      const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
+      if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+    }
+  if (starts_out && lane == 0) starts_out[act] = start;
+  __syncwarp();
+}
+
 // Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same
 // results as the reference's time-indexed SGS; every branch is warp-uniform
 // and every shared access goes through a precomputed 32-bit shared address.
 // The next activity's order entry and record depend only on the order, so
-// they are loaded one activity ahead; precedence is pushed (finish time ->
+// they are loaded one activity ahead (loop unrolled by two so the prefetch
+// needs no register copies); precedence is pushed (finish time ->
 // successors' es) so an activity's es is a single load.
 //   a_ord:  the warp's order [n] (already swapped)      a_info: records [n]
 //   a_push: edge targets of the push graph               a_req:  packed demand
@@ -86,76 +174,22 @@ __device__ __forceinline__ int sgs_time_warp(uint32_t a_info, uint32_t a_push, u
   for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
   int cmax = 0, hw = 0;
-  int act = static_cast<int>(lds32(a_ord));
-  int4 rec = lds128(a_info + 16 * act);
-  for (int pos = 0; pos < n; ++pos) {
-    const int esv = static_cast<int>(lds32(a_es + 4 * act));
-    const int act_n = static_cast<int>(lds32(a_ord + 4 * min(pos + 1, n - 1)));
-    const int4 rec_n = lds128(a_info + 16 * act_n);
-    const int dur = rec.x;
-    const uint32_t r0 = static_cast<uint32_t>(rec.y);
-    const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
-    int start = esv;
-    if (dur > 0 && (r0 | r1) != 0) {
-      if (esv < hw) {
-        const int sh = rec.w;
-        int t0 = esv, carry = 0;
-        for (;;) {
-          const int t = t0 + lane;
-          uint32_t w0 = cap0, w1 = cap1;
-          if (t < hw) {
-            w0 = lds32(a_tau + 4 * W * t);
-            if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
-          }
-          const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
-          const uint32_t m = __ballot_sync(FULL_MASK, ok);
-          const int z = __ffs(~m) - 1;              // -1 when all 32 slots fit
-          if (carry + (z < 0 ? 32 : z) >= dur) {
-            start = t0 - carry;
-            break;
-          }
-          if (dur <= 32) {
-            const uint32_t y = window_runs(m, sh);
-            if (y) {
-              start = t0 + __ffs(y) - 1;
-              break;
-            }
-          }
-          carry = z < 0 ? carry + 32 : __clz(~m);
-          t0 += 32;
-          if (t0 >= H) {  // cannot happen for valid instances
-            start = H;
-            if (lane == 0) set_err(err, DE_NO_WINDOW);
-            break;
-          }
-        }
-      }
-      const int fin = start + dur;
-      if (start > hw)
-        for (int t = hw + lane; t < start; t += 32) {
-          sts32(a_tau + 4 * W * t, cap0);
-          if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
-        }
-      for (int t = start + lane; t < fin; t += 32) {
-        const uint32_t adr = a_tau + 4 * W * t;
-        const bool old = t < hw;
-        sts32(adr, (old ? lds32(adr) : cap0) - r0);
-        if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
-      }
-      hw = max(hw, fin);
-    }
-    const int fin = start + dur;
-    cmax = max(cmax, fin);
-    const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-    for (int e = lane; e < ecnt; e += 32) {
-      const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
-      if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-    }
-    if (starts_out && lane == 0) starts_out[act] = start;
-    act = act_n;
-    rec = rec_n;
-    __syncwarp();
+  int act_a = static_cast<int>(lds32(a_ord));
+  int4 rec_a = lds128(a_info + 16 * act_a);
+  int pos = 0;
+  for (; pos + 1 < n; pos += 2) {
+    const int act_b = static_cast<int>(lds32(a_ord + 4 * (pos + 1)));
+    const int4 rec_b = lds128(a_info + 16 * act_b);
+    time_step_warp<W>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es, hw, cmax,
+                      starts_out, err);
+    act_a = static_cast<int>(lds32(a_ord + 4 * min(pos + 2, n - 1)));
+    rec_a = lds128(a_info + 16 * act_a);
+    time_step_warp<W>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es, hw, cmax,
+                      starts_out, err);
   }
+  if (pos < n)
+    time_step_warp<W>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es, hw, cmax,
+                      starts_out, err);
   return cmax;
 }
 
