@@ -149,6 +149,14 @@ int rcpsp_export_elites(const RcpspSolveArgs *args, int32_t *elites, int32_t *el
 int rcpsp_diversify_batch(const int32_t *blob, int32_t *orders, int batch, int phi_steps,
                           uint64_t *rng, void *stream);
 
+/* Single-step resource-state operations on the reference's state layouts
+ * (kernels.py:68-146 via evaluator.py:171-209): op 0 = cap_earliest_start,
+ * 1 = cap_update (arg = start), 2 = time_earliest_start (arg = es_prec),
+ * 3 = time_update (arg = start).  state: CAP int32 [m][R_max], TIME int32
+ * [m][H+1] (updated in place); out[0] receives the earliest start. */
+int rcpsp_state_op(const int32_t *blob, int op, int32_t *state, int act, int arg, int32_t *out,
+                   int32_t *err, void *stream);
+
 /* Parity probes of the device RNG and Eq. 8 (assigned_iterations,
  * cooperation.py:233-243). ops: [k*2] (kind, n) with kind 0 = integers(n),
  * 1 = permutation(arange(n)); out receives the draws back to back. */

@@ -78,6 +78,12 @@ def lib():
         L.oracle_pcg_integers.argtypes = [_u64p, ctypes.c_int64]
         L.oracle_pcg_integers.restype = ctypes.c_int64
         L.oracle_pcg_permute.argtypes = [_u64p, _i32p, _c_int]
+        L.oracle_cap_earliest_start.argtypes = [_i32p, _c_int, _i32p, _c_int, _i32p, _c_int]
+        L.oracle_cap_update.argtypes = [_i32p, _c_int, _i32p, _c_int, _i32p, _i32p, _c_int,
+                                        _c_int, _c_int]
+        L.oracle_time_earliest_start.argtypes = [_i32p, _c_int, _c_int, _i32p, _c_int, _c_int,
+                                                 _c_int, _c_int]
+        L.oracle_time_update.argtypes = [_i32p, _c_int, _c_int, _i32p, _c_int, _c_int, _c_int]
         _lib = L
     return _lib
 
@@ -292,6 +298,41 @@ def orchestrate(inst, total_iters: int, workers: int = 1, seed: int = 0, mode: i
             p += int(ln)
         res["traces"] = pieces
     return res
+
+
+def cap_earliest_start(inst, levels: np.ndarray, act: int) -> int:
+    """kernels.cap_earliest_start (kernels.py:68-78) on levels [m][R_max]."""
+    oi = _oi(inst)
+    return int(lib().oracle_cap_earliest_start(np.ascontiguousarray(levels, np.int32).reshape(-1),
+                                               levels.shape[1], oi.capacities, oi.m,
+                                               oi.demands.reshape(-1), int(act)))
+
+
+def cap_update(inst, levels: np.ndarray, act: int, start: int) -> None:
+    """kernels.cap_update (kernels.py:81-110); levels updated in place."""
+    oi = _oi(inst)
+    flat = np.ascontiguousarray(levels, np.int32).reshape(-1)
+    buf = np.zeros(levels.shape[1], np.int32)
+    lib().oracle_cap_update(flat, levels.shape[1], oi.capacities, oi.m, oi.demands.reshape(-1),
+                            buf, int(act), int(start), int(oi.durations[act]))
+    levels[...] = flat.reshape(levels.shape)
+
+
+def time_earliest_start(inst, free: np.ndarray, act: int, es_prec: int) -> int:
+    """kernels.time_earliest_start (kernels.py:117-136) on free [m][H+1]."""
+    oi = _oi(inst)
+    return int(lib().oracle_time_earliest_start(
+        np.ascontiguousarray(free, np.int32).reshape(-1), free.shape[1], oi.m,
+        oi.demands.reshape(-1), int(act), int(es_prec), int(oi.durations[act]), oi.horizon))
+
+
+def time_update(inst, free: np.ndarray, act: int, start: int) -> None:
+    """kernels.time_update (kernels.py:139-146); free updated in place."""
+    oi = _oi(inst)
+    flat = np.ascontiguousarray(free, np.int32).reshape(-1)
+    lib().oracle_time_update(flat, free.shape[1], oi.m, oi.demands.reshape(-1), int(act),
+                             int(start), int(oi.durations[act]))
+    free[...] = flat.reshape(free.shape)
 
 
 def pcg_integers(state: np.ndarray, n: int) -> int:

@@ -65,6 +65,7 @@ _SIGNATURES = {
     "rcpsp_rng_probe": ([_vp, _vp, _i, _vp, _vp], _i),
     "rcpsp_eq8_probe": ([_vp, _i, _vp, _vp], _i),
     "rcpsp_smem_probe": ([_i, _i, _i, _vp, _vp], _i),
+    "rcpsp_state_op": ([_vp, _i, _vp, _i, _i, _vp, _vp, _vp], _i),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
 
 #include "../../include/rcpsp_tabu_b200.h"
@@ -229,6 +230,70 @@ __global__ void __launch_bounds__(1024) k_smem_probe(int iters, int* sink) {
     idx = (idx + 128 + (acc.x & 1)) & 2047;
   }
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x7fffffff) sink[0] = 1;
+}
+
+// Single-step resource-state operations on the reference's state layouts
+// (evaluator.py:30-107 wrappers of kernels.py:68-146), executed with the
+// same device functions the SGS uses.  state: CAP -> int32 [m][R_max];
+// TIME -> int32 [m][H+1] free units (packed into lane words in shared
+// memory for the warp window search, unpacked back after an update).
+enum StateOp { OP_CAP_ES = 0, OP_CAP_UPDATE = 1, OP_TIME_ES = 2, OP_TIME_UPDATE = 3 };
+
+template <int W>
+__global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, int op, int* state,
+                                                 int act, int arg, int* out, int* err) {
+  int* smem = dsm;
+  SInst I;
+  const int used = align4(stage_instance(blob, smem, I));
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int m = I.m, R = I.rmax, H = I.H, dur = I.dur[act];
+  const int* dem = I.dem + act * m;
+  if (op == OP_CAP_ES || op == OP_CAP_UPDATE) {
+    if (lane == 0) {
+      if (op == OP_CAP_ES) {
+        out[0] = cap_es(state, 1, dem, I.cap, m, R);
+      } else {
+        cap_commit(state, smem + used, 1, dem, I.cap, m, R, arg, dur);
+        out[0] = 0;
+      }
+    }
+    return;
+  }
+  // TIME: pack [m][H+1] into lane words
+  const int lb = blob[B_LB], lanes = 32 / lb;
+  const uint32_t lmask = lb == 8 ? 0xffu : 0xffffu;
+  uint32_t* tau = reinterpret_cast<uint32_t*>(smem + used);
+  for (int t = lane; t <= H; t += 32)
+    for (int w = 0; w < W; ++w) {
+      uint32_t word = 0;
+      for (int k = w * lanes; k < min(m, (w + 1) * lanes); ++k) {
+        const int v = state[k * (H + 1) + t];
+        if (v < 0 || static_cast<uint32_t>(v) > (lmask >> 1)) set_err(err, DE_BAD_BLOB);
+        word |= (static_cast<uint32_t>(v) & lmask) << (lb * (k - w * lanes));
+      }
+      tau[t * W + w] = word;
+    }
+  __syncwarp();
+  const uint32_t r0 = I.req[act * W], r1 = W == 2 ? I.req[act * W + 1] : 0u;
+  const uint32_t cap0 = I.capw[0], cap1 = W == 2 ? I.capw[1] : 0u;
+  if (op == OP_TIME_ES) {
+    int start = arg;  // dur == 0 or es_prec >= H: the reference returns es_prec
+    if (dur > 0 && arg < H)
+      start = warp_window<W>(sa(tau), H + 1, H, r0, r1, cap0, cap1, I.hi, arg, dur,
+                             window_shifts(dur), nullptr);
+    if (lane == 0) out[0] = start;
+    return;
+  }
+  int hw = H + 1;
+  if (dur > 0) warp_commit<W>(sa(tau), hw, arg, dur, r0, r1, cap0, cap1);
+  __syncwarp();
+  for (int t = lane; t <= H; t += 32)
+    for (int k = 0; k < m; ++k) {
+      const int w = k / lanes;
+      state[k * (H + 1) + t] = static_cast<int>((tau[t * W + w] >> (lb * (k % lanes))) & lmask);
+    }
+  if (lane == 0) out[0] = 0;
 }
 
 // =========================================================================
@@ -954,6 +1019,25 @@ int rcpsp_diversify_batch(const int32_t* blob, int32_t* orders, int batch, int p
 int rcpsp_smem_probe(int blocks, int threads, int iters, int32_t* sink, void* stream) {
   k_smem_probe<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
   return launch_check("k_smem_probe");
+}
+
+int rcpsp_state_op(const int32_t* blob, int op, int32_t* state, int act, int arg, int32_t* out,
+                   int32_t* err, void* stream) {
+  Hdr h;
+  if (read_hdr(blob, h)) return -1;
+  if (op < OP_CAP_ES || op > OP_TIME_UPDATE) return fail("unknown state op");
+  if (act < 0 || act >= h.n) return fail("activity out of range");
+  const size_t words = ((inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3) +
+                       static_cast<size_t>(std::max((h.H + 1) * h.W, h.rmax)) + 4;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (h.W == 2) {
+    if (set_smem(k_state_op<2>, words * 4)) return -1;
+    k_state_op<2><<<1, 32, words * 4, s>>>(blob, op, state, act, arg, out, err);
+  } else {
+    if (set_smem(k_state_op<1>, words * 4)) return -1;
+    k_state_op<1><<<1, 32, words * 4, s>>>(blob, op, state, act, arg, out, err);
+  }
+  return launch_check("k_state_op");
 }
 
 int rcpsp_rng_probe(uint64_t* state, const int32_t* ops, int k, int32_t* out, void* stream) {

@@ -67,6 +67,70 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
   return y;
 }
 
+// Earliest window (kernels.py:117-136) for one activity, whole warp:
+// first t >= esv with [t, t+dur) fitting, slots >= hw at capacity, t+dur <= H.
+// Each round tests 32 slots and resolves the window branch-free: the run
+// carried from the previous round, else the first run of `dur` ones.
+template <int W>
+__device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
+                                           uint32_t r1, uint32_t cap0, uint32_t cap1,
+                                           uint32_t hi, int esv, int dur, int sh, int* err) {
+  const int lane = threadIdx.x & 31;
+  int t0 = esv, carry = 0;
+  for (;;) {
+    const int t = t0 + lane;
+    uint32_t w0 = cap0, w1 = cap1;
+    if (t < hw) {
+      w0 = lds32(a_tau + 4 * W * t);
+      if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
+    }
+    const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
+    const uint32_t m = __ballot_sync(FULL_MASK, ok);
+    const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
+    if (carry + tz >= dur) return t0 - carry;
+    if (dur <= 32) {
+      const uint32_t y = window_runs(m, sh);
+      if (y) return t0 + __ffs(y) - 1;
+    }
+    carry = tz == 32 ? carry + 32 : __clz(~m);
+    t0 += 32;
+    if (t0 >= H) {  // cannot happen for valid instances
+      if (lane == 0) set_err(err, DE_NO_WINDOW);
+      return H;
+    }
+  }
+}
+
+// Book an activity on [start, start+dur) (kernels.py:139-146): materialise
+// [hw, start) at capacity, subtract the packed demand, advance hw.
+template <int W>
+__device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, int dur,
+                                            uint32_t r0, uint32_t r1, uint32_t cap0,
+                                            uint32_t cap1) {
+  const int lane = threadIdx.x & 31;
+  const int fin = start + dur;
+  if (start > hw)
+    for (int t = hw + lane; t < start; t += 32) {
+      sts32(a_tau + 4 * W * t, cap0);
+      if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+    }
+  const int t = start + lane;  // one slot per lane (a loop only for dur > 32)
+  if (lane < dur) {
+    const uint32_t adr = a_tau + 4 * W * t;
+    const bool old = t < hw;
+    sts32(adr, (old ? lds32(adr) : cap0) - r0);
+    if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+  }
+  if (dur > 32)
+    for (int tt = t + 32; tt < fin; tt += 32) {
+      const uint32_t adr = a_tau + 4 * W * tt;
+      const bool old = tt < hw;
+      sts32(adr, (old ? lds32(adr) : cap0) - r0);
+      if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+    }
+  hw = max(hw, fin);
+}
+
 // One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
 template <int W>
 __device__ __forceinline__ void time_step_warp(int act, const int4& rec, uint32_t a_push,
@@ -81,62 +145,9 @@ __device__ __forceinline__ void time_step_warp(int act, const int4& rec, uint32_
   const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
   int start = esv;
   if (dur > 0 && (r0 | r1) != 0) {
-    if (esv < hw) {
-      const int sh = rec.w;
-      int t0 = esv, carry = 0;
-      for (;;) {
-        const int t = t0 + lane;
-        uint32_t w0 = cap0, w1 = cap1;
-        if (t < hw) {
-          w0 = lds32(a_tau + 4 * W * t);
-          if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
-        }
-        const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
-        const uint32_t m = __ballot_sync(FULL_MASK, ok);
-        const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
-        if (carry + tz >= dur) {
-          start = t0 - carry;
-          break;
-        }
-        if (dur <= 32) {
-          const uint32_t y = window_runs(m, sh);
-          if (y) {
-            start = t0 + __ffs(y) - 1;
-            break;
-          }
-        }
-        carry = tz == 32 ? carry + 32 : __clz(~m);
-        t0 += 32;
-        if (t0 >= H) {  // cannot happen for valid instances
-          start = H;
-          if (lane == 0) set_err(err, DE_NO_WINDOW);
-          break;
-        }
-      }
-    }
-    const int fin = start + dur;
-    if (start > hw)
-      for (int t = hw + lane; t < start; t += 32) {
-        sts32(a_tau + 4 * W * t, cap0);
-        if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
-      }
-    {  // subtract the demand on [start, fin): one slot per lane
-      const int t = start + lane;
-      if (lane < dur) {
-        const uint32_t adr = a_tau + 4 * W * t;
-        const bool old = t < hw;
-        sts32(adr, (old ? lds32(adr) : cap0) - r0);
-        if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
-      }
-      if (dur > 32)
-        for (int tt = t + 32; tt < fin; tt += 32) {
-          const uint32_t adr = a_tau + 4 * W * tt;
-          const bool old = tt < hw;
-          sts32(adr, (old ? lds32(adr) : cap0) - r0);
-          if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
-        }
-    }
-    hw = max(hw, fin);
+    if (esv < hw)
+      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur, rec.w, err);
+    warp_commit<W>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
   cmax = max(cmax, fin);
@@ -296,6 +307,50 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
   return cmax;
 }
 
+// Eq. 7 (kernels.py:68-78): earliest start the capacity-indexed state allows.
+// c: the state, element (k, i) at c[(k*R + i)*SK]
+__device__ __forceinline__ int cap_es(const int* c, int SK, const int* dem, const int* cap, int m,
+                                      int R) {
+  int es_res = 0;
+  for (int k = 0; k < m; ++k) {
+    const int req = dem[k];
+    if (req > 0) es_res = max(es_res, c[(k * R + cap[k] - req) * SK]);
+  }
+  return es_res;
+}
+
+// Alg. 4 (kernels.py:81-110), quirks preserved: consume req*dur effort per
+// resource with the shifted-copy buffer cb[i*SK].
+__device__ __forceinline__ void cap_commit(int* c, int* cb, int SK, const int* dem,
+                                           const int* cap, int m, int R, int start, int dur) {
+  for (int k = 0; k < m; ++k) {
+    const int req = dem[k];
+    int effort = req * dur;
+    if (effort <= 0) continue;
+    int* ck = c + (k * R) * SK;
+    const int capk = cap[k];
+    int copy_idx = 0;
+    int new_time = start + dur;
+    for (int res_idx = 0; effort > 0 && res_idx < capk; ++res_idx) {
+      const int cv = ck[res_idx * SK];
+      if (cv < new_time) {
+        if (copy_idx >= req) new_time = cb[(copy_idx - req) * SK];
+        const int fl = cv < start ? start : cv;
+        const int diff = new_time - fl;
+        if (effort - diff > 0) {
+          effort -= diff;
+          cb[copy_idx * SK] = cv;
+          ++copy_idx;
+          ck[res_idx * SK] = new_time;
+        } else {
+          ck[res_idx * SK] = fl + effort;
+          effort = 0;
+        }
+      }
+    }
+  }
+}
+
 // Capacity-indexed SGS, one thread per schedule.
 //   st: the warp's interleaved scratch; word j of slot `slot` at st[j*SK + slot]
 //       (SK = lanes sharing the scratch, 32 normally: conflict-free)
@@ -317,40 +372,8 @@ __device__ __forceinline__ int sgs_cap_thread(const SInst& I, int* __restrict__ 
     const int act = act_at(pos);
     const int dur = I.dur[act];
     const int* dem = I.dem + act * m;
-    // Eq. 7 (kernels.py:68-78)
-    int es_res = 0;
-    for (int k = 0; k < m; ++k) {
-      const int req = dem[k];
-      if (req > 0) es_res = max(es_res, c[(k * R + I.cap[k] - req) * SK]);
-    }
-    const int start = max(es[act * SK], es_res);
-    // Alg. 4 (kernels.py:81-110), quirks preserved
-    for (int k = 0; k < m; ++k) {
-      const int req = dem[k];
-      int effort = req * dur;
-      if (effort <= 0) continue;
-      int* ck = c + (k * R) * SK;
-      const int capk = I.cap[k];
-      int copy_idx = 0;
-      int new_time = start + dur;
-      for (int res_idx = 0; effort > 0 && res_idx < capk; ++res_idx) {
-        const int cv = ck[res_idx * SK];
-        if (cv < new_time) {
-          if (copy_idx >= req) new_time = cb[(copy_idx - req) * SK];
-          const int fl = cv < start ? start : cv;
-          const int diff = new_time - fl;
-          if (effort - diff > 0) {
-            effort -= diff;
-            cb[copy_idx * SK] = cv;
-            ++copy_idx;
-            ck[res_idx * SK] = new_time;
-          } else {
-            ck[res_idx * SK] = fl + effort;
-            effort = 0;
-          }
-        }
-      }
-    }
+    const int start = max(es[act * SK], cap_es(c, SK, dem, I.cap, m, R));
+    cap_commit(c, cb, SK, dem, I.cap, m, R, start, dur);
     const int fin = start + dur;
     cmax = max(cmax, fin);
     for (int e = push_ptr[act]; e < push_ptr[act + 1]; ++e) {

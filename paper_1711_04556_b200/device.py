@@ -307,6 +307,28 @@ def eq8_probe(quads: np.ndarray) -> np.ndarray:
     return out.cpu().numpy()
 
 
+STATE_OPS = {"cap_es": 0, "cap_update": 1, "time_es": 2, "time_update": 3}
+
+
+def state_op(inst: ProjectInstance, op: str, state: np.ndarray, act: int, arg: int = 0) -> int:
+    """One resource-state step on the GPU (rcpsp_state_op); `state` (the
+    reference's CAP [m][R_max] or TIME [m][H+1] int32 layout) is updated in
+    place for the *_update ops.  Returns the earliest start for the *_es ops."""
+    torch = _torch()
+    L = _native.lib()
+    di = device_instance(inst)
+    d_state = to_dev(np.ascontiguousarray(state, np.int32))
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    check(L.rcpsp_state_op(ptr(di.blob), STATE_OPS[op], ptr(d_state), int(act), int(arg),
+                           ptr(out), ptr(err), stream_handle()), "rcpsp_state_op")
+    if int(err.cpu()[0]):
+        raise ValueError("resource state holds values outside the packed lane range")
+    if op.endswith("update"):
+        state[...] = d_state.cpu().numpy().reshape(state.shape)
+    return int(out.cpu()[0])
+
+
 def smem_bandwidth(iters: int = 4096, reps: int = 5) -> float:
     """Measured shared-memory load bandwidth of this GPU in GB/s (best of reps)."""
     torch = _torch()

@@ -106,6 +106,22 @@ def test_assigned_iterations_matches_reference(golden):
     assert oracle.assigned_iterations(100, 10**9, 1000, 100) == 160
 
 
+def test_single_step_goldens():
+    """Fig. 4 and the gap cases (reference test_evaluator.py:49-160)."""
+    from paper_1711_04556_b200 import make_instance
+    inst = make_instance("fig4", [0, 3, 0], [7], [[0], [3], [0]], [[1], [2], []])
+    lv = np.array([[7, 7, 5, 5, 5, 5, 4]], np.int32)
+    assert oracle.cap_earliest_start(inst, lv, 1) == 5
+    oracle.cap_update(inst, lv, 1, 5)
+    assert lv[0].tolist() == [8, 8, 8, 7, 7, 5, 4]
+    gap = make_instance("g", [0, 5, 3, 5, 0], [2], [[0], [2], [2], [0], [0]],
+                        [[1, 2, 3], [4], [4], [4], []])
+    free = np.full((1, 14), 2, np.int32)
+    oracle.time_update(gap, free, 1, 5)
+    assert oracle.time_earliest_start(gap, free, 2, 0) == 0
+    assert oracle.time_earliest_start(gap, free, 2, 4) == 10
+
+
 def test_touch_counter_positive(ginst):
     inst = ginst["genr120s0"]
     order = np.arange(inst.n_activities)
