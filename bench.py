@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--epochs", type=int, default=4, help="elite-exchange epochs (N > 1)")
     ap.add_argument("--group", type=int, default=None, help="TIME lanes per schedule")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
+    ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
+                    help="evaluation mode: the static rules (default) or forced")
     ap.add_argument("--no-steal", action="store_true",
                     help="fixed worker-to-instance mapping (no tail balancing)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -211,7 +213,10 @@ def main() -> None:
     from paper_1711_04556_b200.population import EliteExchange, run_epochs
 
     insts = synth.benchmark_batch(args.config, args.instances)
-    modes = [int(decide_static(extract_features(x))) for x in insts]
+    if args.mode == "rule":
+        modes = [int(decide_static(extract_features(x))) for x in insts]
+    else:
+        modes = [1 if args.mode == "time" else 0] * len(insts)
     p = SearchParams.defaults_for(insts[0].n_activities, total_iters=args.iters,
                                   workers=args.workers, seed=1000 * rank)
     cfg = SolveConfig(total_iters=p.total_iters, workers=p.workers, pool_size=p.pool_size,
