@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
     ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
                     help="evaluation mode: the static rules (default) or forced")
+    ap.add_argument("--full-sgs", action="store_true",
+                    help="evaluate every swap by a full SGS (no prefix reuse)")
     ap.add_argument("--no-steal", action="store_true",
                     help="fixed worker-to-instance mapping (no tail balancing)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -222,7 +224,7 @@ def main() -> None:
     cfg = SolveConfig(total_iters=p.total_iters, workers=p.workers, pool_size=p.pool_size,
                       tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
                       phi_max=p.phi_max, seed=p.seed, group=args.group, threads=args.threads,
-                      steal=not args.no_steal)
+                      steal=not args.no_steal, full_sgs=args.full_sgs)
     solver = BatchSolver(insts, modes, cfg)
     solver.upload()
     stream = torch.cuda.current_stream()

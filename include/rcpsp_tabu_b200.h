@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 2
+#define RCPSP_ABI_VERSION 3
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -80,6 +80,9 @@ typedef struct RcpspSolveArgs {
     int64_t steal;              /* 1 = a worker whose instance has spent its
                                  * budget moves on to instances with budget
                                  * left (balances the batch tail; B > 1) */
+    int64_t full_sgs;           /* 1 = evaluate every swap by a full SGS;
+                                 * 0 (default) = group 32 reuses the base
+                                 * order's schedule prefix (same makespans) */
 } RcpspSolveArgs;
 
 int rcpsp_abi_version(void);

@@ -15,7 +15,7 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 
@@ -45,7 +45,7 @@ class RcpspSolveArgs(ctypes.Structure):
         ("moves_buf", _vp), ("cmax_buf", _vp), ("nbhd_max", ctypes.c_int64), ("err", _vp),
         ("h_max", ctypes.c_int64), ("e_max", ctypes.c_int64), ("m_max", ctypes.c_int64),
         ("rmax_max", ctypes.c_int64), ("words", ctypes.c_int64), ("group", ctypes.c_int64),
-        ("threads", ctypes.c_int64), ("steal", ctypes.c_int64),
+        ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
     ]
 
 

@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
   cta_setup(c, A.blob + A.blob_off[iid], smem, plan, static_cast<int>(A.delta), T,
             A.moves_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max,
             A.cmax_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max, A.err);
+  c.inc = A.full_sgs == 0;
   const size_t wid = static_cast<size_t>(iid) * B + wk;  // this worker's rng / stats slot
   int64_t* st = A.w_stats + wid * 16;
   int* wtrace = A.collect_trace ? A.w_trace + wid * A.trace_cap : nullptr;

@@ -21,7 +21,8 @@ namespace rt {
 
 enum Scal {
   SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
-  SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_WORDS = 32
+  SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_BASEC,
+  SC_CTR, SC_WORDS = 32
 };
 
 struct CtaCtx {
@@ -34,6 +35,7 @@ struct CtaCtx {
   int* rs;         // [n] row start of the flat neighbourhood (rows 1..n-2)
   int* best;       // [n] best order of the chunk
   int* rowc;       // [n] diversify row counts
+  int* bst;        // [n] start of each activity in the current order's schedule
   uint32_t* tabu_list;  // [T] packed (u << 16) | v, 0 = empty slot
   uint32_t* tabu_cnt;   // [(n*(delta+1)+1)/2] two 16-bit counters per word
   int* red;        // [72] reduction scratch
@@ -41,6 +43,7 @@ struct CtaCtx {
   int* evs;        // evaluation scratch (per warp)
   int warp_words;  // evaluation scratch words per warp
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
+  bool inc;        // TIME G = 32: reuse the current order's schedule prefix
   uint32_t* moves_buf;  // global [nbhd] compacted moves
   int* cmax_buf;        // global [nbhd] makespans
   int* err;
@@ -268,6 +271,112 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
   }
 }
 
+__device__ __forceinline__ int atom_inc_shared(uint32_t a) {
+  int old;
+  asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(a) : "memory");
+  return old;
+}
+
+// TIME, one warp per schedule, reusing the current order's schedule.
+//
+// For the swap (u, v) (u < v) the swapped order equals the current one on
+// positions < u, so the serial SGS state after those positions is the
+// current schedule's.  Each warp keeps that prefix state -- profile below
+// the mark hw_pre, es pushed by the prefix (es_pre), its makespan -- and
+// extends it with the known starts `bst` as its u grows: moves are handed
+// out in increasing (lexicographic) index order by a shared counter, so a
+// warp's u never decreases.  A move then schedules positions u.. only, and
+// undoes its bookings below hw_pre afterwards.
+//
+// Convergence: the SGS state after position p is a function of the starts
+// of the activities at positions <= p.  If every activity at positions
+// u..v starts where it does in the current schedule (the activities there
+// are the same set), the state after v equals the current one and the rest
+// of the schedule -- hence the makespan -- is the current schedule's.
+//
+// Every makespan equals the full SGS's (kernels.py:152-194); the work per
+// move shrinks from n activity steps to the suffix.
+//   o_bst: [n] starts of the current schedule; base_cmax: its makespan
+//   o_ctr: shared move counter (zeroed by the caller)
+//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n]
+template <int W>
+__device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
+                                                   int o_bst, int o_ctr, int o_evs, uint32_t cap0,
+                                                   uint32_t cap1, uint32_t hi, int n, int H,
+                                                   const uint32_t* __restrict__ moves,
+                                                   int* __restrict__ cmax_out, int n_feas,
+                                                   int warp_words, int base_cmax, int* err) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* ws = dsm + o_evs + warp * warp_words;
+  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_req = sa(dsm + o_req),
+                 a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
+                 a_tau = sa(ws), a_es = sa(ws + (H + 1) * W), a_esp = a_es + 4 * n;
+  for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
+  __syncwarp();
+  int up = 0, hw_pre = 0, cm_pre = 0;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atom_inc_shared(a_ctr);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_feas) break;
+    const uint32_t mv = moves[idx];
+    const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    // ---- extend the prefix to positions < u with the known starts
+    for (; up < u; ++up) {
+      const int act = static_cast<int>(lds32(a_base + 4 * up));
+      const int4 rec = lds128(a_info + 16 * act);
+      const int s = static_cast<int>(lds32(a_bst + 4 * act));
+      const uint32_t r0 = static_cast<uint32_t>(rec.y);
+      const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
+      if (rec.x > 0 && (r0 | r1) != 0) warp_commit<W>(a_tau, hw_pre, s, rec.x, r0, r1, cap0, cap1);
+      const int fin = s + rec.x;
+      cm_pre = max(cm_pre, fin);
+      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+      for (int e = lane; e < ecnt; e += 32) {
+        const uint32_t adr = a_esp + 4 * lds32(a_push + 4 * (e0 + e));
+        if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+      }
+      __syncwarp();
+    }
+    for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
+    __syncwarp();
+    // ---- the suffix u.. of the swapped order
+    int hw = hw_pre, cm = cm_pre, p = u;
+    bool div = false;
+    int act = static_cast<int>(lds32(a_base + 4 * v));
+    int4 rec = lds128(a_info + 16 * act);
+    for (; p < n; ++p) {
+      const int pn = p + 1 < n ? p + 1 : p;
+      const int qn = pn == v ? u : pn;
+      const int act_n = static_cast<int>(lds32(a_base + 4 * qn));
+      const int4 rec_n = lds128(a_info + 16 * act_n);
+      const int s = time_step_warp<W, true>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
+                                            a_es, hw, cm, nullptr, err);
+      if (!div) {
+        div = s != static_cast<int>(lds32(a_bst + 4 * act));
+        if (!div && p >= v) break;  // converged: the current schedule from here on
+      }
+      act = act_n;
+      rec = rec_n;
+    }
+    if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
+    // ---- undo the suffix's bookings below hw_pre
+    const int last = p < n ? p : n - 1;
+    for (int q = u; q <= last; ++q) {
+      const int qq = q == u ? v : (q == v ? u : q);
+      const int a = static_cast<int>(lds32(a_base + 4 * qq));
+      const int4 r = lds128(a_info + 16 * a);
+      const uint32_t r0 = static_cast<uint32_t>(r.y);
+      const uint32_t r1 = W == 2 ? lds32(a_req + 8 * a + 4) : 0u;
+      if (r.x > 0 && (r0 | r1) != 0) {
+        const int s = static_cast<int>(lds32(a_es + 4 * a));
+        if (s < hw_pre) warp_uncommit<W>(a_tau, hw_pre, s, r.x, r0, r1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // TIME, G = 16 / 8 lanes per schedule (S = 32/G schedules per warp)
 template <int G, int W>
 __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req, int o_base,
@@ -326,9 +435,30 @@ template <int MODE, int G, int W>
 __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
   if constexpr (MODE == MODE_TIME) {
     if constexpr (G == 32) {
-      eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
-                           soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
-                           c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
+      if (c.inc) {
+        // the current order's schedule (starts -> bst), then prefix-reusing moves
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp == 0) {
+          uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
+          int* es = c.evs + (c.I.H + 1) * W;
+          const int cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req), c.I.capw[0],
+                                          W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H,
+                                          sa(tau), sa(es), sa(c.base), c.bst, c.err);
+          if (lane == 0) {
+            c.scal[SC_BASEC] = cm;
+            c.scal[SC_CTR] = 0;
+          }
+        }
+        __syncthreads();
+        eval_moves_time32_inc<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
+                                 soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0],
+                                 W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, c.moves_buf,
+                                 c.cmax_buf, n_feas, c.warp_words, c.scal[SC_BASEC], c.err);
+      } else {
+        eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
+                             soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
+                             c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
+      }
     } else {
       eval_moves_split<G, W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
                              soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
@@ -478,7 +608,7 @@ __device__ void cta_diversify(CtaCtx& c, int* work, int steps, Pcg64& rng) {
 // ------------------------------------------------------ shared-memory plan
 
 struct SmemPlan {
-  int inst, base, pos, msp, mpp, rs, best, rowc, tabu_list, tabu_cnt, red, scal, evs;
+  int inst, base, pos, msp, mpp, rs, best, rowc, bst, tabu_list, tabu_cnt, red, scal, evs;
   int warp_words, total, cap_lanes;
 };
 
@@ -502,6 +632,7 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.rs = off; off += a4(n);
   p.best = off; off += a4(n);
   p.rowc = off; off += a4(n);
+  p.bst = off; off += a4(n);
   p.tabu_list = off; off += a4(T > 0 ? T : 1);
   p.tabu_cnt = off; off += a4((n * (delta + 1) + 1) / 2);
   p.red = off; off += 72;
@@ -526,6 +657,8 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.rs = smem + p.rs;
   c.best = smem + p.best;
   c.rowc = smem + p.rowc;
+  c.bst = smem + p.bst;
+  c.inc = true;
   c.tabu_list = reinterpret_cast<uint32_t*>(smem + p.tabu_list);
   c.tabu_cnt = reinterpret_cast<uint32_t*>(smem + p.tabu_cnt);
   c.red = smem + p.red;

@@ -131,9 +131,27 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
   hw = max(hw, fin);
 }
 
-// One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
+// Inverse of warp_commit below the mark `hw_keep`: give the demand on
+// [start, min(start+dur, hw_keep)) back.  Slots at or above hw_keep need no
+// undo -- resetting the high-water mark to hw_keep makes them implicit
+// capacity again.
 template <int W>
-__device__ __forceinline__ void time_step_warp(int act, const int4& rec, uint32_t a_push,
+__device__ __forceinline__ void warp_uncommit(uint32_t a_tau, int hw_keep, int start, int dur,
+                                              uint32_t r0, uint32_t r1) {
+  const int lane = threadIdx.x & 31;
+  const int e = min(start + dur, hw_keep);
+  for (int t = start + lane; t < e; t += 32) {
+    const uint32_t adr = a_tau + 4 * W * t;
+    sts32(adr, lds32(adr) + r0);
+    if (W == 2) sts32(adr + 4, lds32(adr + 4) + r1);
+  }
+}
+
+// One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
+// Returns the start; REC also records it in es[act] (dead once the activity
+// is scheduled), where the prefix-reusing evaluator's undo finds it.
+template <int W, bool REC = false>
+__device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t a_push,
                                                uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                                uint32_t hi, int H, uint32_t a_tau,
                                                uint32_t a_es, int& hw, int& cmax,
@@ -162,7 +180,9 @@ __device__ __forceinline__ void time_step_warp(int act, const int4& rec, uint32_
       if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
     }
   if (starts_out && lane == 0) starts_out[act] = start;
+  if (REC && lane == 0) sts32(a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
+  return start;
 }
 
 // Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same

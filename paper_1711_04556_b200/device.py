@@ -264,7 +264,17 @@ def run_chunk_batch(inst: ProjectInstance, mode: int, delta: int, orders, tabu_l
     _raise_dev_err(err)
     st = stats.cpu().numpy()
     tl_out = d_tabu.cpu().numpy().view(np.uint32)
+    # the last iteration's compacted neighbourhood and its makespans
+    n_last = st[:, 1] if int(budget.max()) == 1 else None
+    mv = mbuf.cpu().numpy().view(np.uint32)
+    cm = cbuf.cpu().numpy()
+    last = None
+    if n_last is not None:
+        last = [(np.stack([(mv[b, :k] >> 16).astype(np.int32),
+                           (mv[b, :k] & 0xFFFF).astype(np.int32)], 1).reshape(-1, 2),
+                 cm[b, :k].copy()) for b, k in enumerate(n_last)]
     return dict(order=d_ord.cpu().numpy(), best_order=best.cpu().numpy(), stats=st,
+                neighbourhood=last,
                 trace=(trace.cpu().numpy() if collect_trace else None),
                 tabu=np.stack([(tl_out >> 16).astype(np.int32),
                                (tl_out & 0xFFFF).astype(np.int32)], -1),
@@ -378,6 +388,7 @@ class SolveConfig:
     group: int | None = None
     threads: int = 0          # 0 = auto (two CTAs per SM when they fit)
     steal: bool = True        # B > 1: idle workers help instances with budget left
+    full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluator
 
     @property
     def block_iters(self) -> int:
@@ -524,6 +535,7 @@ class BatchSolver:
         a.group = cfg.group if cfg.group is not None else pick_group(self.n_max)
         a.threads = cfg.threads
         a.steal = int(cfg.steal and cfg.workers > 1 and not cfg.collect_trace)
+        a.full_sgs = int(cfg.full_sgs)
         return a
 
     def pool_init(self, stream=None) -> None:

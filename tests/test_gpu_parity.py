@@ -125,6 +125,62 @@ def test_run_chunk_golden(golden, ginst, group):
         assert res["tabu"][0].tolist() == rec["out_tabu_list"]
 
 
+def _swap_rows(order, moves):
+    out = np.repeat(order[None], len(moves), 0)
+    r = np.arange(len(moves))
+    out[r, moves[:, 0]] = order[moves[:, 1]]
+    out[r, moves[:, 1]] = order[moves[:, 0]]
+    return out
+
+
+def _check_neighbourhood(inst, orders, mode, delta, group, key):
+    """One run_chunk iteration per order: every evaluated swap's makespan ==
+    the oracle's full SGS of the swapped order (kernels.py:350-362)."""
+    S = len(orders)
+    T = 8
+    tl = [np.zeros((T, 2), np.int32) for _ in range(S)]
+    cm, _ = oracle.evaluate_batch(inst, orders, mode)
+    res = device.run_chunk_batch(inst, mode, delta, orders, tl, [0] * S, 1, 0, cm, cm, 0,
+                                 group=group)
+    nb = oracle.neighborhood(inst.n_activities, delta)
+    for b in range(S):
+        moves, got = res["neighbourhood"][b]
+        want_moves = oracle.filter_moves(inst, orders[b], nb)
+        assert moves.tolist() == want_moves.tolist(), key
+        if len(moves):
+            want, _ = oracle.evaluate_batch(inst, _swap_rows(orders[b], moves), mode)
+            assert got.tolist() == want.tolist(), (key, b)
+
+
+@pytest.mark.parametrize("cfg", ["j30", "j60", "j120", "act300"])
+def test_neighbourhood_makespans_vs_oracle(cfg):
+    """Prefix-reusing (group 32) and full-SGS (group 16) neighbourhood
+    evaluation inside the search kernel, every move checked."""
+    rng = np.random.default_rng(21)
+    for inst in synth.benchmark_batch(cfg, 2, first_seed=40):
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(6)])
+        # also orders the search actually visits: FBI-improved ones are denser
+        for group in (32, 16):
+            _check_neighbourhood(inst, orders, 1, 60, group, (cfg, group))
+
+
+def test_neighbourhood_makespans_shapes():
+    """Wide packings (W = 2), long durations, tiny instances, delta = n."""
+    rng = np.random.default_rng(23)
+    for seed in range(24):
+        m = int(rng.integers(1, 9))
+        cap_hi = int(rng.choice([6, 20, 127, 300]))
+        if m > 4 and cap_hi > 127:
+            cap_hi = 127
+        inst = synth.random_instance(int(rng.integers(3, 50)), m, seed=100 + seed,
+                                     cap_lo=max(1, cap_hi // 3), cap_hi=cap_hi,
+                                     max_dur=int(rng.choice([3, 10, 40])),
+                                     demand_density=float(rng.choice([0.3, 1.0])))
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(4)])
+        delta = int(rng.choice([3, 30, inst.n_activities]))
+        _check_neighbourhood(inst, orders, 1, delta, 32, seed)
+
+
 def test_run_chunk_batch_independent(ginst):
     """Several searches in one launch give the same results as one each."""
     inst = ginst["genr60s0"]
@@ -309,3 +365,18 @@ def test_merge_elites_model(ginst):
         assert got_o[i, :, :n].tolist() == po
         assert int(got_b[i]) == b
         assert s.best_order.cpu().numpy()[i, :n].tolist() == bo
+
+
+def test_full_sgs_equals_prefix_reuse():
+    """The whole batch solve gives identical trajectories with and without
+    prefix reuse (B = 1 per instance, traces compared)."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts = synth.benchmark_batch("j120", 3, first_seed=7)
+    out = []
+    for full in (False, True):
+        cfg = SolveConfig(total_iters=120, workers=1, pool_size=8, tabu_size=800, delta=60,
+                          phi_steps=20, phi_max=3, seed=1, collect_trace=True, full_sgs=full)
+        r = BatchSolver(insts, [1] * 3, cfg).run()
+        out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
+                    [[t.tolist() for t in tr] for tr in r.traces]))
+    assert out[0] == out[1]
