@@ -298,7 +298,9 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n]
+//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n] | log [n]
+// The log lists the suffix activities booked below hw_pre (the only ones the
+// undo has to visit).
 template <int W>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
@@ -310,7 +312,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   int* ws = dsm + o_evs + warp * warp_words;
   const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
-                 a_tau = sa(ws), a_es = sa(ws + (H + 1) * W), a_esp = a_es + 4 * n;
+                 a_tau = sa(ws), a_es = sa(ws + (H + 1) * W), a_esp = a_es + 4 * n,
+                 a_log = a_esp + 4 * n;
   for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
   __syncwarp();
   int up = 0, hw_pre = 0, cm_pre = 0;
@@ -341,7 +344,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
     __syncwarp();
     // ---- the suffix u.. of the swapped order
-    int hw = hw_pre, cm = cm_pre, p = u;
+    int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
     int act = static_cast<int>(lds32(a_base + 4 * v));
     int4 rec = lds128(a_info + 16 * act);
@@ -352,6 +355,10 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       const int4 rec_n = lds128(a_info + 16 * act_n);
       const int s = time_step_warp<W, true>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                             a_es, hw, cm, nullptr, err);
+      if (s < hw_pre) {  // may have booked below hw_pre: undo later
+        if (lane == 0) sts32(a_log + 4 * nlog, static_cast<uint32_t>(act));
+        ++nlog;
+      }
       if (!div) {
         div = s != static_cast<int>(lds32(a_bst + 4 * act));
         if (!div && p >= v) break;  // converged: the current schedule from here on
@@ -361,16 +368,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     }
     if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
     // ---- undo the suffix's bookings below hw_pre
-    const int last = p < n ? p : n - 1;
-    for (int q = u; q <= last; ++q) {
-      const int qq = q == u ? v : (q == v ? u : q);
-      const int a = static_cast<int>(lds32(a_base + 4 * qq));
+    __syncwarp();
+    for (int k = 0; k < nlog; ++k) {
+      const int a = static_cast<int>(lds32(a_log + 4 * k));
       const int4 r = lds128(a_info + 16 * a);
       const uint32_t r0 = static_cast<uint32_t>(r.y);
       const uint32_t r1 = W == 2 ? lds32(a_req + 8 * a + 4) : 0u;
       if (r.x > 0 && (r0 | r1) != 0) {
-        const int s = static_cast<int>(lds32(a_es + 4 * a));
-        if (s < hw_pre) warp_uncommit<W>(a_tau, hw_pre, s, r.x, r0, r1);
+        warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(lds32(a_es + 4 * a)), r.x, r0, r1);
       }
     }
     __syncwarp();
@@ -614,7 +619,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 3 * n : (32 / G) * ((H + 1) * W + 2 * n);
   return cap_lanes * cap_thread_words(n, m, rmax);
 }
 
