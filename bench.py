@@ -64,6 +64,8 @@ def parse():
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-quality", action="store_true",
+                    help="skip the fixed-wall-clock CPM-deviation comparison")
     return ap.parse_args()
 
 
@@ -156,7 +158,7 @@ def cpu_sample(cfg: str, iters: int, target_s: float, threads: int, seed: int = 
         if wall >= target_s or k >= 64:
             break
     return {"value": evals / wall, "evaluations": evals, "wall": wall, "instances": k,
-            "cpm_dev": float(np.mean(devs)), "iters": iters}
+            "cpm_dev": float(np.mean(devs)), "iters": iters, "threads": threads}
 
 
 def run_reference(args, ws: int, rank: int) -> None:
@@ -196,6 +198,32 @@ def run_reference(args, ws: int, rank: int) -> None:
 
 # ---------------------------------------------------------------------------
 # B200 arm
+
+def quality_leg(args, insts, modes, cb: dict, iter_rate: float) -> dict:
+    """Mean % deviation from the CPM bound at a fixed wall-clock budget: the
+    CPU sample's instances (first K seeds) solved on the GPU within the wall
+    time the reference algorithm took for them on all host cores.  The GPU
+    budget per instance is calibrated from the timed steps' iteration rate."""
+    import torch
+    from paper_1711_04556_b200 import SearchParams
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    K = int(cb["instances"])
+    qi, qm = insts[:K], modes[:K]
+    workers = max(1, (2 * args.instances) // K)      # same CTA count as the timed steps
+    budget = int(0.7 * iter_rate * cb["wall"] / K)   # headroom for pool init / tail
+    p = SearchParams.defaults_for(qi[0].n_activities, total_iters=budget, workers=workers, seed=0)
+    cfg = SolveConfig(total_iters=budget, workers=workers, pool_size=p.pool_size,
+                      tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
+                      phi_max=p.phi_max, seed=0, group=args.group, threads=args.threads)
+    res = BatchSolver(qi, qm, cfg).run()
+    torch.cuda.synchronize()
+    dev = float(np.mean(100.0 * (res.best_cmax - res.critical_path) / res.critical_path))
+    return {"wall_budget_s": cb["wall"], "instances": K,
+            "cpu": {"cpm_dev": cb["cpm_dev"], "iters_per_instance": cb["iters"],
+                    "kind": "port", "workers_per_instance": cb.get("threads")},
+            "gpu": {"cpm_dev": dev, "iters_per_instance": budget,
+                    "workers_per_instance": workers, "device_s": res.device_ms * 1e-3}}
+
 
 def main() -> None:
     args = parse()
@@ -256,6 +284,7 @@ def main() -> None:
 
     launches0 = solver.launches
     step_ms, search_ms, evals, search_evals, devs = [], [], 0, 0, []
+    sgs_steps, iters_done = 0, 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             solver.reset()
@@ -274,6 +303,8 @@ def main() -> None:
             res = solver.collect()
             evals += int(res.evaluations.sum())
             search_evals += int((res.evaluations - res.pool_evaluations).sum())
+            sgs_steps += res.sgs_steps
+            iters_done += int(res.iterations.sum())
             devs.append(float(np.mean(100.0 * (res.best_cmax - res.critical_path)
                                       / res.critical_path)))
     launches = solver.launches - launches0
@@ -325,6 +356,7 @@ def main() -> None:
     # roofline of the dominant kernel (k_solve): algorithmic bytes of the
     # schedules it evaluated / its measured duration, vs measured SMEM bandwidth
     W = work_per_schedule(args.config)
+    n_act = insts[0].n_activities
     mode_key = "time" if modes.count(1) >= modes.count(0) else "cap"
     bytes_per_sched = W[mode_key]["bytes"]
     s_ms = sum(search_ms)
@@ -355,12 +387,18 @@ def main() -> None:
                    "pool_size": p.pool_size, "delta": p.delta, "tabu_size": p.tabu_size,
                    "modes": {"TIME": modes.count(1), "CAPACITY": modes.count(0)},
                    "epochs": epochs, "cpm_dev": float(np.mean(devs)),
+                   "evaluations_per_step": evals // args.steps,
+                   "iterations_per_step": iters_done // args.steps,
                    "l2": "256 MiB buffer written between timed steps",
                    "parallelism": f"{ws} independent populations" + (
                        ", NCCL all_gather elite exchange" if ws > 1 else "")},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "k_solve", "bytes_per_schedule": bytes_per_sched,
+                     "bytes_basis": "reference full-SGS element touches x 4 B per evaluated "
+                                    "schedule (profiles/work_per_schedule.json)",
+                     "sgs_steps_per_schedule": sgs_steps / max(1, search_evals),
+                     "executed_step_fraction": sgs_steps / max(1, search_evals * n_act),
                      "peak_source": "measured in this run: rcpsp_smem_probe (LDS.128 stream)",
                      "hbm_peak_gbs": hbm_peak},
         "clocks": clk,
@@ -377,6 +415,8 @@ def main() -> None:
             "sample": f"{cb['instances']} {args.config} Gen-R instances (seeds 0..), "
                       f"I_total={cb['iters']}, {cores} worker threads each, "
                       f"{cb['wall']:.1f} s; cpm_dev {cb['cpm_dev']:.2f}%"}
+        if not args.no_quality:
+            line["quality"] = quality_leg(args, insts, modes, cb, iters_done / (tot_ms * 1e-3))
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

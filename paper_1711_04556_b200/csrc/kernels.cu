@@ -31,7 +31,7 @@ enum WsField {
 };
 enum WkField {
   WK_ITERS = 0, WK_EVALS = 1, WK_EXCH = 2, WK_DIV = 3, WK_FORCED = 4, WK_CHUNKS = 5,
-  WK_TRACE = 6, WK_T0 = 7, WK_T1 = 8
+  WK_TRACE = 6, WK_T0 = 7, WK_T1 = 8, WK_STEPS = 9
 };
 
 thread_local std::string g_err;
@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
       st[WK_EXCH] += 1;
       st[WK_DIV] += needs_div ? 1 : 0;
       st[WK_FORCED] += o.forced;
+      st[WK_STEPS] += o.steps;
     }
     if (wtrace) {
       if (tid == 0 && chunks < A.chunk_cap) wchunks[chunks] = o.iters;

@@ -22,7 +22,7 @@ namespace rt {
 enum Scal {
   SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
   SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_BASEC,
-  SC_CTR, SC_WORDS = 32
+  SC_CTR, SC_STEPS, SC_WORDS = 32
 };
 
 struct CtaCtx {
@@ -316,7 +316,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                  a_log = a_esp + 4 * n;
   for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
   __syncwarp();
-  int up = 0, hw_pre = 0, cm_pre = 0;
+  int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = atom_inc_shared(a_ctr);
@@ -367,6 +367,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       rec = rec_n;
     }
     if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
+    steps += (p < n ? p + 1 : n) - u;
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     for (int k = 0; k < nlog; ++k) {
@@ -380,6 +381,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     }
     __syncwarp();
   }
+  // SGS activity steps of this warp: suffixes + prefix extension
+  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
 }
 
 // TIME, G = 16 / 8 lanes per schedule (S = 32/G schedules per warp)
@@ -452,6 +455,7 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
           if (lane == 0) {
             c.scal[SC_BASEC] = cm;
             c.scal[SC_CTR] = 0;
+            c.scal[SC_STEPS] = c.I.n;  // the current order's schedule
           }
         }
         __syncthreads();
@@ -505,6 +509,7 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
 struct ChunkOut {
   int iters, improved, local_best, cur, forced;
   long long evals;
+  long long steps;  // SGS activity steps spent on the neighbourhoods
 };
 
 // kernels.py:316-385.  c.base holds the order (mutated in place), the tabu
@@ -514,7 +519,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
                                   int best_known_cmax, int floor_cmax, int* trace) {
   const int tid = threadIdx.x, n = c.I.n;
   int local_best = start_cmax, cur = start_cmax, iters = 0, forced = 0;
-  long long evals = 0;
+  long long evals = 0, steps = 0;
   for (int it = 0; it < budget; ++it) {
     const int n_feas = cta_filter(c);
     ++iters;
@@ -524,6 +529,8 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     }
     cta_eval_moves<MODE, G, W>(c, n_feas);
     evals += n_feas;
+    steps += (MODE == MODE_TIME && G == 32 && c.inc) ? c.scal[SC_STEPS]
+                                                    : static_cast<long long>(n_feas) * n;
     const int asp = best_known_cmax < local_best ? best_known_cmax : local_best;
     unsigned ka = 0xffffffffu, kl = 0xffffffffu;
     for (int idx = tid; idx < n_feas; idx += blockDim.x) {
@@ -562,6 +569,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
   ChunkOut o;
   o.iters = iters;
   o.evals = evals;
+  o.steps = steps;
   o.improved = local_best < adopted_cmax ? 1 : 0;
   o.local_best = local_best;
   o.cur = cur;

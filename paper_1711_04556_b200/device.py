@@ -35,7 +35,7 @@ WS_FIELDS = dict(cursor=0, total=1, planned=2, consumed=3, stop=4, best=5, best_
                  pool_evals=8, t0=9, t1=10, iterations=11, evaluations=12, exchanges=13,
                  diversifications=14, forced=15)
 WK_FIELDS = dict(iterations=0, evaluations=1, exchanges=2, diversifications=3, forced=4,
-                 chunks=5, trace_len=6, t0=7, t1=8)
+                 chunks=5, trace_len=6, t0=7, t1=8, sgs_steps=9)
 
 KEY_LIMIT = 1 << 16   # selection key packs (C_max << 16 | rank)
 
@@ -413,6 +413,7 @@ class BatchResult:
     inst_wall_s: np.ndarray          # [I] per-instance search span (globaltimer)
     traces: list = field(default_factory=list)   # per instance: list of chunk arrays
     n_launches: int = 0
+    sgs_steps: int = 0               # activity steps the workers' neighbourhood SGS ran
 
 
 class BatchSolver:
@@ -603,7 +604,7 @@ class BatchSolver:
             forced=hdr[:, WS_FIELDS["forced"]].astype(np.int64),
             stopped=hdr[:, WS_FIELDS["stop"]].astype(bool),
             device_ms=device_ms, search_ms=search_ms, inst_wall_s=span, traces=traces,
-            n_launches=self.launches)
+            n_launches=self.launches, sgs_steps=int(ws[:, :, WK_FIELDS["sgs_steps"]].sum()))
 
     def run(self, stream=None) -> BatchResult:
         """upload -> pool init -> search -> collect, timed with CUDA events."""
