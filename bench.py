@@ -235,9 +235,16 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # one rank per GPU; BENCH_DIST_BACKEND=gloo (testing only) lets several
+    # ranks share one GPU to exercise the N > 1 path on a single-GPU box
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     from paper_1711_04556_b200 import SearchParams, decide_static, extract_features, synth
     from paper_1711_04556_b200.device import (BatchSolver, SolveConfig, smem_bandwidth)
     from paper_1711_04556_b200.population import EliteExchange, run_epochs
@@ -285,7 +292,7 @@ def main() -> None:
     launches0 = solver.launches
     step_ms, search_ms, evals, search_evals, devs = [], [], 0, 0, []
     sgs_steps, iters_done = 0, 0
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         for _ in range(args.steps):
             solver.reset()
             flush.fill_(1)                       # L2 flush between timed steps
