@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
     ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
                     help="evaluation mode: the static rules (default) or forced")
+    ap.add_argument("--cap-group", type=int, default=32, choices=[32, 1],
+                    help="CAPACITY evaluator: 32 = warp per schedule, 1 = thread per schedule")
     ap.add_argument("--full-sgs", action="store_true",
                     help="evaluate every swap by a full SGS (no prefix reuse)")
     ap.add_argument("--no-steal", action="store_true",
@@ -259,7 +261,8 @@ def main() -> None:
     cfg = SolveConfig(total_iters=p.total_iters, workers=p.workers, pool_size=p.pool_size,
                       tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
                       phi_max=p.phi_max, seed=p.seed, group=args.group, threads=args.threads,
-                      steal=not args.no_steal, full_sgs=args.full_sgs)
+                      steal=not args.no_steal, full_sgs=args.full_sgs,
+                      cap_group=args.cap_group)
     solver = BatchSolver(insts, modes, cfg)
     solver.upload()
     stream = torch.cuda.current_stream()

@@ -96,6 +96,18 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
                                 err);
     }
     if (active && lane_g == 0) cmax[b] = cm;
+  } else if constexpr (G == 32) {
+    const int words = cap_warp_words(n, I.m, I.rmax) + n;
+    int* scr = scratch + warp * words;
+    int* ord = scr + cap_warp_words(n, I.m, I.rmax);
+    const int b = blockIdx.x * nw + warp;
+    if (b >= batch) return;
+    for (int p = lane; p < n; p += 32) ord[p] = orders[static_cast<size_t>(b) * n + p];
+    __syncwarp();
+    const int cm = sgs_cap_warp(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.dem), I.cap, n,
+                                I.m, cap_row_stride(I.rmax), sa(scr), sa(ord),
+                                starts ? starts + static_cast<size_t>(b) * n : nullptr);
+    if (lane == 0) cmax[b] = cm;
   } else {
     const int L = cap_lanes;
     const int words = cap_thread_words(n, I.m, I.rmax) + n;
@@ -334,10 +346,9 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
                           W == 2 ? I.capw[1] : 0u, I.hi, I.n, I.H, sa(scr),
                           sa(scr + (I.H + 1) * W), sa(ord), starts, err);
   } else {
-    cm = 0;
-    if ((threadIdx.x & 31) == 0)
-      cm = sgs_cap_thread(I, scr, 1, 0, [&](int p) { return ord[p]; }, pp, pd, starts);
-    cm = __shfl_sync(FULL_MASK, cm, 0);
+    (void)pp;
+    cm = sgs_cap_warp(sa(reverse ? I.info_r : I.info_f), sa(pd), sa(I.dem), I.cap, I.n, I.m,
+                      cap_row_stride(I.rmax), sa(scr), sa(ord), starts);
   }
   __syncwarp();
   return cm;
@@ -387,7 +398,7 @@ __host__ __device__ inline int pool_entry_words(int mode, int n, int m, int H, i
                                                 int rmax) {
   const int inst = (inst_smem_words(n, m, e, W) + 3) & ~3;
   const int arrays = 8 * n;  // ord, s1, s2, key, indeg, ready, border/forder, final
-  const int ev = mode == MODE_TIME ? (H + 1) * W + n : cap_thread_words(n, m, rmax);
+  const int ev = mode == MODE_TIME ? (H + 1) * W + n : cap_warp_words(n, m, rmax);
   return inst + arrays + ev + 8;
 }
 
@@ -794,7 +805,7 @@ bool fit_plan_limit(int mode, int G, int W, int n, int m, int H, int e, int rmax
                     int T, int want_threads, size_t limit, int min_threads, SmemPlan& p,
                     int& threads) {
   for (threads = want_threads; threads >= min_threads; threads -= 32) {
-    for (int lanes = 32; lanes >= (mode == MODE_CAPACITY ? 1 : 32); --lanes) {
+    for (int lanes = 32; lanes >= (mode == MODE_CAPACITY && G == 1 ? 1 : 32); --lanes) {
       p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes);
       if (static_cast<size_t>(p.total) * 4 <= limit) return true;
     }
@@ -831,8 +842,13 @@ int launch_check(const char* what) { return cuda_check(cudaGetLastError(), what)
 
 // dispatch helper: calls f.template operator()<MODE,G,W>()
 template <class Fn>
-int dispatch(int mode, int group, int words, Fn&& f) {
-  if (mode == MODE_CAPACITY) return f.template operator()<MODE_CAPACITY, 32, 1>();
+int dispatch(int mode, int group, int words, int m, Fn&& f) {
+  if (mode == MODE_CAPACITY) {
+    // group 1: one thread per schedule; otherwise one warp per schedule (lane = resource)
+    if (group == 1) return f.template operator()<MODE_CAPACITY, 1, 1>();
+    if (m > 32) return fail("CAPACITY group 32 supports at most 32 resources (use group 1)");
+    return f.template operator()<MODE_CAPACITY, 32, 1>();
+  }
   if (mode != MODE_TIME) return fail("mode must be 0 (CAPACITY) or 1 (TIME)");
   if (words != 1 && words != 2) return fail("TIME packing needs 1 or 2 words per slot");
   if (group == 32) return words == 1 ? f.template operator()<MODE_TIME, 32, 1>() : f.template operator()<MODE_TIME, 32, 2>();
@@ -867,13 +883,15 @@ int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int b
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t limit = smem_optin();
   const size_t inst = (inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3;
-  return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
+  return dispatch(mode, group, h.W, h.m, [&]<int MODE, int G, int W>() -> int {
     // largest warp count (<= 8) and CAP lane count (<= 32) whose scratch fits
     int nw = 8, lanes = 32;
     size_t words = 0;
     for (;;) {
       if (MODE == MODE_TIME)
         words = inst + static_cast<size_t>(nw) * (32 / G) * ((h.H + 1) * W + 2 * h.n);
+      else if (G == 32)
+        words = inst + static_cast<size_t>(nw) * (cap_warp_words(h.n, h.m, h.rmax) + h.n);
       else
         words = inst + static_cast<size_t>(nw) * lanes * (cap_thread_words(h.n, h.m, h.rmax) + h.n);
       if (words * 4 <= limit) break;
@@ -881,7 +899,7 @@ int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int b
       else if (MODE == MODE_CAPACITY && lanes > 1) --lanes;
       else return fail("evaluation scratch does not fit in shared memory");
     }
-    const int per_block = MODE == MODE_TIME ? nw * (32 / G) : nw * lanes;
+    const int per_block = MODE == MODE_TIME ? nw * (32 / G) : (G == 32 ? nw : nw * lanes);
     const int blocks = (batch + per_block - 1) / per_block;
     auto k = k_eval_batch<MODE, G, W>;
     if (set_smem(k, words * 4)) return -1;
@@ -916,10 +934,10 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
   if (read_hdr(blob, h)) return -1;
   if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return dispatch(mode, group, h.W, [&]<int MODE, int G, int W>() -> int {
+  return dispatch(mode, group, h.W, h.m, [&]<int MODE, int G, int W>() -> int {
     SmemPlan p;
     int nt;
-    if (!fit_search_plan(MODE, G, W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads, p, nt))
+    if (!fit_search_plan(MODE, G, h.W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads, p, nt))
       return fail("search state does not fit in shared memory");
     auto k = k_run_chunk<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
@@ -973,11 +991,11 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   if (threads % 32 || threads < 0 || threads > 512) return fail("threads must be 0 (auto) or 32..512, x32");
   if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words),
+  return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words), static_cast<int>(A.m_max),
                   [&]<int MODE, int G, int W>() -> int {
     SmemPlan p;
     int nt;
-    if (!fit_search_plan(MODE, G, W, static_cast<int>(A.n_max), static_cast<int>(A.m_max),
+    if (!fit_search_plan(MODE, G, static_cast<int>(A.words), static_cast<int>(A.n_max), static_cast<int>(A.m_max),
                          static_cast<int>(A.h_max), static_cast<int>(A.e_max),
                          static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
                          static_cast<int>(A.tabu_size), threads, p, nt))

@@ -419,6 +419,76 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req,
   }
 }
 
+// CAP, one warp per schedule (sgs.cuh: cap_step_warp), reusing the current
+// order's schedule prefix like eval_moves_time32_inc.  Alg. 4 is not
+// invertible and its state depends on the update order (not only on the set
+// of starts), so there is no undo and no convergence exit: each move copies
+// the prefix state (c_pre, es_pre) and schedules positions u..n-1.  With
+// reuse == false the prefix stays empty (full SGS of every swapped order).
+//   per-warp scratch: c [m*rs] | cb [rs] | es [n] | c_pre [m*rs] | es_pre [n]
+__device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_dem, int o_cap,
+                                                 int o_base, int o_bst, int o_ctr, int o_evs,
+                                                 int n, int m, int rs,
+                                                 const uint32_t* __restrict__ moves,
+                                                 int* __restrict__ cmax_out, int n_feas,
+                                                 int warp_words, bool reuse) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mr = m * rs;
+  const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
+  const uint32_t a_c = a_scr, a_cb = a_c + 4 * mr, a_es = a_cb + 4 * rs, a_cp = a_es + 4 * n,
+                 a_esp = a_cp + 4 * mr;
+  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
+                 a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr);
+  const int capk = lane < m ? dsm[o_cap + lane] : 0;
+  for (int j = lane; j < mr; j += 32) sts32(a_cp + 4 * j, 0);
+  for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
+  __syncwarp();
+  int up = 0, cm_pre = 0, steps = 0;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atom_inc_shared(a_ctr);
+    idx = __shfl_sync(FULL_MASK, idx, 0);
+    if (idx >= n_feas) break;
+    const uint32_t mv = moves[idx];
+    const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    const int u0 = reuse ? u : 0;
+    // ---- extend the prefix state to positions < u0 with the known starts
+    for (; up < u0; ++up) {
+      const int act = static_cast<int>(lds32(a_base + 4 * up));
+      const int4 rec = lds128(a_info + 16 * act);
+      const int st = static_cast<int>(lds32(a_bst + 4 * act));
+      if (rec.x > 0) {
+        const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
+        cap_commit_all(a_cp, a_cb, rs, m, capk, req, st, rec.x);
+      }
+      const int fin = st + rec.x;
+      cm_pre = max(cm_pre, fin);
+      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
+      for (int e = lane; e < ecnt; e += 32) {
+        const uint32_t adr = a_esp + 4 * lds32(a_push + 4 * (e0 + e));
+        if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+      }
+      __syncwarp();
+    }
+    for (int j = lane; j < mr; j += 32) sts32(a_c + 4 * j, lds32(a_cp + 4 * j));
+    for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
+    __syncwarp();
+    // ---- positions u0.. of the swapped order
+    int cm = cm_pre;
+    for (int p = u0; p < n; ++p) {
+      const int q = p == u ? v : (p == v ? u : p);
+      const int act = static_cast<int>(lds32(a_base + 4 * q));
+      const int4 rec = lds128(a_info + 16 * act);
+      const int esv = static_cast<int>(lds32(a_es + 4 * act));
+      cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_cb, a_push, rec.z & 0xffff,
+                    rec.z >> 16, a_es, cm);
+    }
+    if (lane == 0) cmax_out[idx] = cm;
+    steps += n - u0;
+  }
+  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
+}
+
 // CAP, one thread per schedule
 __device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_evs,
                                             const uint32_t* __restrict__ moves,
@@ -473,6 +543,23 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
                              soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
                              c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, c.err);
     }
+  } else if constexpr (G == 32) {
+    // the current order's schedule (starts -> bst), then one warp per move
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+      if (c.inc)
+        sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
+                     cap_row_stride(c.I.rmax), sa(c.evs), sa(c.base), c.bst);
+      if (lane == 0) {
+        c.scal[SC_CTR] = 0;
+        c.scal[SC_STEPS] = c.inc ? c.I.n : 0;
+      }
+    }
+    __syncthreads();
+    eval_moves_cap_warp(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.dem), soff(c.I.cap),
+                        soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.n,
+                        c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
+                        c.warp_words, c.inc);
   } else {
     eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
                    c.warp_words, c.cap_lanes);
@@ -492,6 +579,9 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
       cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req), c.I.capw[0],
                             W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, sa(tau), sa(es),
                             sa(ord), nullptr, c.err);
+    } else if constexpr (G == 32) {
+      cm = sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
+                        cap_row_stride(c.I.rmax), sa(c.evs), sa(ord), nullptr);
     } else {
       cm = 0;
       if (lane == 0)
@@ -529,8 +619,8 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     }
     cta_eval_moves<MODE, G, W>(c, n_feas);
     evals += n_feas;
-    steps += (MODE == MODE_TIME && G == 32 && c.inc) ? c.scal[SC_STEPS]
-                                                    : static_cast<long long>(n_feas) * n;
+    steps += (G == 32 && (MODE == MODE_CAPACITY || c.inc))
+                 ? c.scal[SC_STEPS] : static_cast<long long>(n_feas) * n;
     const int asp = best_known_cmax < local_best ? best_known_cmax : local_best;
     unsigned ka = 0xffffffffu, kl = 0xffffffffu;
     for (int idx = tid; idx < n_feas; idx += blockDim.x) {
@@ -628,6 +718,7 @@ struct SmemPlan {
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 3 * n : (32 / G) * ((H + 1) * W + 2 * n);
+  if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return cap_lanes * cap_thread_words(n, m, rmax);
 }
 

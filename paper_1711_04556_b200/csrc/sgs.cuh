@@ -409,4 +409,140 @@ __host__ __device__ __forceinline__ int cap_thread_words(int n, int m, int rmax)
   return m * rmax + rmax + n;  // per lane
 }
 
+// ---------------------------------------------------------------------------
+// Warp-cooperative capacity-indexed SGS (group 32): one warp per schedule,
+// lane k < m owns resource k -- its row of the state c_k and of the copy
+// buffer -- so Eq. 7's max over resources is one REDUX and the m Alg. 4
+// updates run side by side.  Rows are `rs` words apart (rmax rounded up to
+// odd: the m rows fall in distinct banks).
+//   scratch: c [m*rs] | cb [rs] | es [n]
+
+__host__ __device__ __forceinline__ int cap_row_stride(int rmax) { return rmax | 1; }
+
+__host__ __device__ __forceinline__ int cap_warp_words(int n, int m, int rmax) {
+  return (m + 1) * cap_row_stride(rmax) + n;
+}
+
+// Alg. 4 (kernels.py:81-110) on one resource row from entry i0 on, one
+// lane, quirks preserved.  Entries before i0 are the leading run with
+// c >= start + dur, which the reference's loop skips one by one.
+__device__ __forceinline__ void cap_commit_row(uint32_t a_c, uint32_t a_cb, int capk, int req,
+                                               int start, int dur, int i0 = 0) {
+  int effort = req * dur;
+  if (effort <= 0) return;
+  int copy_idx = 0, new_time = start + dur;
+  for (int i = i0; effort > 0 && i < capk; ++i) {
+    const int cv = static_cast<int>(lds32(a_c + 4 * i));
+    if (cv < new_time) {
+      if (copy_idx >= req) new_time = static_cast<int>(lds32(a_cb + 4 * (copy_idx - req)));
+      const int fl = cv < start ? start : cv;
+      const int diff = new_time - fl;
+      if (effort - diff > 0) {
+        effort -= diff;
+        sts32(a_cb + 4 * copy_idx, static_cast<uint32_t>(cv));
+        ++copy_idx;
+        sts32(a_c + 4 * i, static_cast<uint32_t>(new_time));
+      } else {
+        sts32(a_c + 4 * i, static_cast<uint32_t>(fl + effort));
+        effort = 0;
+      }
+    }
+  }
+}
+
+// Alg. 4 on one resource row, whole warp.  The leading run of entries with
+// c >= start + dur is found with ballots (the row is descending).  If the
+// first entry below start + dur is already free at `start`, so are the next
+// req - 1 (descending row, and Eq. 7 guarantees req entries <= start), and
+// the reference's loop sets exactly those req entries to start + dur -- done
+// by req lanes at once (~90-95 % of updates on the Gen-R configs).  Else
+// lane 0 runs the loop from i0.
+__device__ __forceinline__ void cap_commit_warp(uint32_t a_c, uint32_t a_cb, int capk, int req,
+                                                int start, int dur) {
+  if (req * dur <= 0) return;
+  const int lane = threadIdx.x & 31;
+  const int T = start + dur;
+  int i0 = capk;
+  for (int b = 0; b < capk; b += 32) {
+    const int i = b + lane;
+    const unsigned msk =
+        __ballot_sync(FULL_MASK, i < capk && static_cast<int>(lds32(a_c + 4 * i)) < T);
+    if (msk) {
+      i0 = b + __ffs(msk) - 1;
+      break;
+    }
+  }
+  if (i0 < capk) {
+    const int c0 = static_cast<int>(lds32(a_c + 4 * i0));
+    if (c0 <= start && i0 + req <= capk) {
+      for (int j = lane; j < req; j += 32) sts32(a_c + 4 * (i0 + j), static_cast<uint32_t>(T));
+    } else if (lane == 0) {
+      cap_commit_row(a_c, a_cb, capk, req, start, dur, i0);
+    }
+  }
+  __syncwarp();
+}
+
+// The m resource updates of one activity, one after another, whole warp.
+// req: lane k < m holds resource k's demand.
+__device__ __forceinline__ void cap_commit_all(uint32_t a_c, uint32_t a_cb, int rs, int m,
+                                               int capk, int req, int start, int dur) {
+  for (int k = 0; k < m; ++k) {
+    const int rk = __shfl_sync(FULL_MASK, req, k);
+    const int ck = __shfl_sync(FULL_MASK, capk, k);
+    cap_commit_warp(a_c + 4 * k * rs, a_cb, ck, rk, start, dur);
+  }
+}
+
+// One activity: start = max(es_prec, Eq. 7) (Eq. 7 also for zero durations,
+// as kernels.py:182-186), Alg. 4 per resource, push the finish time.
+//   capk: lane k < m holds resource k's capacity (lanes >= m: 0)
+//   a_c: the state rows (row k at a_c + 4*k*rs); a_cb: copy buffer [rmax]
+template <bool REC = false>
+__device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t a_dem, int m,
+                                             int capk, int rs, uint32_t a_c, uint32_t a_cb,
+                                             uint32_t a_push, int e0, int ecnt, uint32_t a_es,
+                                             int& cmax) {
+  const int lane = threadIdx.x & 31;
+  int req = 0, t = 0;
+  if (lane < m) {
+    req = static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
+    if (req > 0) t = static_cast<int>(lds32(a_c + 4 * (lane * rs + capk - req)));
+  }
+  const int start = max(esv, __reduce_max_sync(FULL_MASK, t));
+  if (dur > 0) cap_commit_all(a_c, a_cb, rs, m, capk, req, start, dur);
+  const int fin = start + dur;
+  cmax = max(cmax, fin);
+  for (int e = lane; e < ecnt; e += 32) {
+    const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
+    if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
+  }
+  if (REC && lane == 0) sts32(a_es + 4 * act, static_cast<uint32_t>(start));
+  __syncwarp();
+  return start;
+}
+
+// Whole schedule of the order at a_ord (one warp); starts_out may be null.
+//   a_info: per-activity records (dur, -, push span, -); a_push: push targets
+__device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, uint32_t a_dem,
+                                            const int* cap, int n, int m, int rs, uint32_t a_scr,
+                                            uint32_t a_ord, int* __restrict__ starts_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t a_c = a_scr, a_cb = a_scr + 4 * m * rs, a_es = a_cb + 4 * rs;
+  for (int j = lane; j < m * rs; j += 32) sts32(a_c + 4 * j, 0);
+  for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
+  __syncwarp();
+  const int capk = lane < m ? cap[lane] : 0;
+  int cmax = 0;
+  for (int pos = 0; pos < n; ++pos) {
+    const int act = static_cast<int>(lds32(a_ord + 4 * pos));
+    const int4 rec = lds128(a_info + 16 * act);
+    const int esv = static_cast<int>(lds32(a_es + 4 * act));
+    const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_cb, a_push,
+                                rec.z & 0xffff, rec.z >> 16, a_es, cmax);
+    if (starts_out && lane == 0) starts_out[act] = s;
+  }
+  return cmax;
+}
+
 }  // namespace rt

@@ -388,7 +388,8 @@ class SolveConfig:
     group: int | None = None
     threads: int = 0          # 0 = auto (two CTAs per SM when they fit)
     steal: bool = True        # B > 1: idle workers help instances with budget left
-    full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluator
+    full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluators
+    cap_group: int = 32       # CAPACITY: 32 = one warp per schedule, 1 = one thread
 
     @property
     def block_iters(self) -> int:
@@ -533,7 +534,10 @@ class BatchSolver:
         a.h_max, a.e_max, a.m_max, a.rmax_max = self.h_max, self.e_max, self.m_max, self.rmax_max
         mode, words = group_key if group_key is not None else (MODE_TIME, 1)
         a.words = words
-        a.group = cfg.group if cfg.group is not None else pick_group(self.n_max)
+        if mode == MODE_CAPACITY:
+            a.group = cfg.cap_group
+        else:
+            a.group = cfg.group if cfg.group is not None else pick_group(self.n_max)
         a.threads = cfg.threads
         a.steal = int(cfg.steal and cfg.workers > 1 and not cfg.collect_trace)
         a.full_sgs = int(cfg.full_sgs)

@@ -14,7 +14,8 @@ from paper_1711_04556_b200 import (EvalMode, SearchParams, check_schedule_feasib
                                    orchestrate, orchestrate_batch, synth)
 from paper_1711_04556_b200.cooperation import initialize_working_set  # noqa: E402
 
-GROUPS = (32, 16, 8)
+GROUPS = (32, 16, 8)        # TIME lanes per schedule
+CAP_GROUPS = (32, 1)        # CAPACITY: warp per schedule / thread per schedule
 
 
 @pytest.mark.parametrize("group", GROUPS)
@@ -58,7 +59,7 @@ def test_eval_fuzz_vs_oracle(cfg, count):
         orders = np.stack([random_topological_order(inst, rng) for _ in range(count // 2)])
         for mode in (0, 1):
             want_c, want_s = oracle.evaluate_batch(inst, orders, mode)
-            for group in GROUPS if mode == 1 else (32,):
+            for group in GROUPS if mode == 1 else CAP_GROUPS:
                 got_c, got_s = device.eval_batch(inst, orders, mode, group=group)
                 assert np.array_equal(got_c, want_c), (cfg, mode, group)
                 assert np.array_equal(got_s, want_s), (cfg, mode, group)
@@ -85,7 +86,8 @@ def test_eval_fuzz_small_shapes():
         orders = np.stack([random_topological_order(inst, rng) for _ in range(60)])
         for mode in (0, 1):
             want_c, want_s = oracle.evaluate_batch(inst, orders, mode)
-            got_c, got_s = device.eval_batch(inst, orders, mode, group=int(rng.choice(GROUPS)))
+            g = int(rng.choice(GROUPS if mode == 1 else CAP_GROUPS))
+            got_c, got_s = device.eval_batch(inst, orders, mode, group=g)
             assert np.array_equal(got_c, want_c), (seed, mode)
             assert np.array_equal(got_s, want_s), (seed, mode)
 
@@ -108,9 +110,11 @@ def test_filter_fuzz_vs_oracle():
                 assert got[b].tolist() == oracle.filter_moves(inst, orders[b], moves).tolist()
 
 
-@pytest.mark.parametrize("group", GROUPS)
+@pytest.mark.parametrize("group", GROUPS + (1,))
 def test_run_chunk_golden(golden, ginst, group):
     for rec in golden["run_chunk"]:
+        if group == 1 and rec["mode"] == 1:
+            continue  # group 1 is the thread-per-schedule CAPACITY evaluator
         inst = ginst[rec["instance"]]
         res = device.run_chunk_batch(inst, rec["mode"], rec["delta"], np.array([rec["order"]]),
                                      [np.array(rec["tabu_list"])], [rec["tabu_head"]],
@@ -162,6 +166,8 @@ def test_neighbourhood_makespans_vs_oracle(cfg):
         # also orders the search actually visits: FBI-improved ones are denser
         for group in (32, 16):
             _check_neighbourhood(inst, orders, 1, 60, group, (cfg, group))
+        for group in CAP_GROUPS if cfg != "act300" else (32,):
+            _check_neighbourhood(inst, orders[:3], 0, 60, group, (cfg, "cap", group))
 
 
 def test_neighbourhood_makespans_shapes():
@@ -179,6 +185,7 @@ def test_neighbourhood_makespans_shapes():
         orders = np.stack([random_topological_order(inst, rng) for _ in range(4)])
         delta = int(rng.choice([3, 30, inst.n_activities]))
         _check_neighbourhood(inst, orders, 1, delta, 32, seed)
+        _check_neighbourhood(inst, orders, 0, delta, int(rng.choice(CAP_GROUPS)), (seed, "cap"))
 
 
 def test_run_chunk_batch_independent(ginst):
@@ -371,12 +378,14 @@ def test_full_sgs_equals_prefix_reuse():
     """The whole batch solve gives identical trajectories with and without
     prefix reuse (B = 1 per instance, traces compared)."""
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
-    insts = synth.benchmark_batch("j120", 3, first_seed=7)
+    insts = synth.benchmark_batch("j120", 4, first_seed=7)
+    modes = [1, 0, 1, 0]
     out = []
-    for full in (False, True):
+    for full, cap_group in ((False, 32), (True, 32), (False, 1)):
         cfg = SolveConfig(total_iters=120, workers=1, pool_size=8, tabu_size=800, delta=60,
-                          phi_steps=20, phi_max=3, seed=1, collect_trace=True, full_sgs=full)
-        r = BatchSolver(insts, [1] * 3, cfg).run()
+                          phi_steps=20, phi_max=3, seed=1, collect_trace=True, full_sgs=full,
+                          cap_group=cap_group)
+        r = BatchSolver(insts, modes, cfg).run()
         out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
                     [[t.tolist() for t in tr] for tr in r.traces]))
-    assert out[0] == out[1]
+    assert out[0] == out[1] == out[2]
