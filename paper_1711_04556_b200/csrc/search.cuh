@@ -298,7 +298,7 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n] | log [n]
+//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n] | log [n] | ord [n]
 // The log lists the suffix activities booked below hw_pre (the only ones the
 // undo has to visit).
 template <int W>
@@ -313,7 +313,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
                  a_tau = sa(ws), a_es = sa(ws + (H + 1) * W), a_esp = a_es + 4 * n,
-                 a_log = a_esp + 4 * n;
+                 a_log = a_esp + 4 * n, a_ord = a_log + 4 * n;
   for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
   __syncwarp();
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
@@ -341,30 +341,40 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       }
       __syncwarp();
     }
+    // ---- the swapped order's suffix u.. (materialised), es from the prefix
+    for (int q = u + lane; q < n; q += 32)
+      sts32(a_ord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
     for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
     __syncwarp();
-    // ---- the suffix u.. of the swapped order
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
-    int act = static_cast<int>(lds32(a_base + 4 * v));
-    int4 rec = lds128(a_info + 16 * act);
-    for (; p < n; ++p) {
-      const int pn = p + 1 < n ? p + 1 : p;
-      const int qn = pn == v ? u : pn;
-      const int act_n = static_cast<int>(lds32(a_base + 4 * qn));
-      const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int s = time_step_warp<W, true>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
-                                            a_es, hw, cm, nullptr, err);
-      if (s < hw_pre) {  // may have booked below hw_pre: undo later
+    // after scheduling `act` at position p: log bookings below hw_pre for the
+    // undo; true once the state provably equals the current schedule's
+    auto after = [&](int act, int st) -> bool {
+      if (st < hw_pre) {
         if (lane == 0) sts32(a_log + 4 * nlog, static_cast<uint32_t>(act));
         ++nlog;
       }
       if (!div) {
-        div = s != static_cast<int>(lds32(a_bst + 4 * act));
-        if (!div && p >= v) break;  // converged: the current schedule from here on
+        div = st != static_cast<int>(lds32(a_bst + 4 * act));
+        if (!div && p >= v) return true;
       }
-      act = act_n;
-      rec = rec_n;
+      return false;
+    };
+    // unrolled by two so the prefetched next activity needs no register copies
+    int act_a = static_cast<int>(lds32(a_ord + 4 * u));
+    int4 rec_a = lds128(a_info + 16 * act_a);
+    for (;;) {
+      const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+      const int4 rec_b = lds128(a_info + 16 * act_b);
+      int st = time_step_warp<W, true>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
+                                       a_es, hw, cm, nullptr, err);
+      if (after(act_a, st) || ++p >= n) break;
+      act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+      rec_a = lds128(a_info + 16 * act_a);
+      st = time_step_warp<W, true>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
+                                   hw, cm, nullptr, err);
+      if (after(act_b, st) || ++p >= n) break;
     }
     if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
     steps += (p < n ? p + 1 : n) - u;
@@ -717,7 +727,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 3 * n : (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return cap_lanes * cap_thread_words(n, m, rmax);
 }

@@ -50,6 +50,10 @@ __device__ __forceinline__ int4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// es[s] = max(es[s], v) as one shared-memory reduction (no return value)
+__device__ __forceinline__ void red_max_shared(uint32_t a, int v) {
+  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
 // wrap-mode funnel shift: y >> (s & 31) (the window shift fields are 5 bits)
 __device__ __forceinline__ uint32_t shr_wrap(uint32_t y, int s) {
@@ -170,15 +174,11 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
   const int fin = start + dur;
   cmax = max(cmax, fin);
   const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-  if (lane < ecnt) {  // push the finish time to the successors' es
-    const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + lane));
-    if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-  }
+  if (lane < ecnt)  // push the finish time to the successors' es
+    red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + lane)), fin);
   if (ecnt > 32)
-    for (int e = lane + 32; e < ecnt; e += 32) {
-      const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
-      if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-    }
+    for (int e = lane + 32; e < ecnt; e += 32)
+      red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
   if (starts_out && lane == 0) starts_out[act] = start;
   if (REC && lane == 0) sts32(a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
