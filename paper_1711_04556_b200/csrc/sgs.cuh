@@ -80,6 +80,10 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
                                            uint32_t hi, int esv, int dur, int sh, int* err) {
   const int lane = threadIdx.x & 31;
+  // lane i tests the window [t0+i, t0+i+dur) inside the round: a candidate
+  // iff it ends in the round, a hit iff dur fitting slots start at bit i
+  const bool cand = lane + dur <= 32;
+  const uint32_t dmask = dur >= 32 ? 0xffffffffu : (1u << dur) - 1u;
   int t0 = esv, carry = 0;
   for (;;) {
     const int t = t0 + lane;
@@ -92,10 +96,8 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
     const uint32_t m = __ballot_sync(FULL_MASK, ok);
     const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
     if (carry + tz >= dur) return t0 - carry;
-    if (dur <= 32) {
-      const uint32_t y = window_runs(m, sh);
-      if (y) return t0 + __ffs(y) - 1;
-    }
+    const uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
+    if (y) return t0 + __ffs(y) - 1;
     carry = tz == 32 ? carry + 32 : __clz(~m);
     t0 += 32;
     if (t0 >= H) {  // cannot happen for valid instances
