@@ -56,8 +56,8 @@ def parse():
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
     ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
                     help="evaluation mode: the static rules (default) or forced")
-    ap.add_argument("--cap-group", type=int, default=32, choices=[32, 1],
-                    help="CAPACITY evaluator: 32 = warp per schedule, 1 = thread per schedule")
+    ap.add_argument("--cap-group", type=int, default=None, choices=[32, 1],
+                    help="CAPACITY evaluator: 32 = warp, 1 = thread per schedule (default auto)")
     ap.add_argument("--full-sgs", action="store_true",
                     help="evaluate every swap by a full SGS (no prefix reuse)")
     ap.add_argument("--no-steal", action="store_true",

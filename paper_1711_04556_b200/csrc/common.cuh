@@ -42,8 +42,8 @@ __device__ __forceinline__ void set_err(int* err, int code) {
 //   z = push span: first edge | (edge count << 16) of the activities whose
 //       earliest start this one's finish time bounds (successors forward,
 //       predecessors for the reversed project),
-//   w = the doubling shifts of the run-of-`dur` window test (5 fields of 5
-//       bits, consumed by wrap-mode funnel shifts; see window_shifts).
+//   w = window_mask(dur): the low `dur` bits, the run the warp evaluator's
+//       window test looks for (the split evaluators derive window_shifts).
 struct SInst {
   int n, m, H, e, W, rmax, cpm;
   uint32_t hi;           // high bit of every packed resource lane (TIME fits test)
@@ -69,6 +69,11 @@ __host__ __device__ __forceinline__ int inst_smem_words(int n, int m, int e, int
 // Fields are 5 bits wide at bit 5*i (every s_i <= 16); a wrap-mode funnel
 // shift uses only the low 5 bits of its amount, so field i is applied as
 // shf.r.wrap(y, 0, packed >> 5*i) without masking.
+// low `d` bits set (all 32 for d >= 32): the window test of the warp evaluator
+__host__ __device__ __forceinline__ uint32_t window_mask(int d) {
+  return d >= 32 ? 0xffffffffu : (1u << d) - 1u;
+}
+
 __host__ __device__ __forceinline__ int window_shifts(int d) {
   int packed = 0, acc = 1;
   for (int i = 0; i < 5; ++i) {
@@ -98,7 +103,7 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
     const int* sp = blob + blob[B_OFF_SPTR];
     const int* pp = blob + blob[B_OFF_PPTR];
     for (int a = threadIdx.x; a < n; a += blockDim.x) {
-      const int d = bd[a], r = br[a * W], sh = window_shifts(d);
+      const int d = bd[a], r = br[a * W], sh = static_cast<int>(window_mask(d));
       inf[a] = make_int4(d, r, sp[a] | ((sp[a + 1] - sp[a]) << 16), sh);
       inf[n + a] = make_int4(d, r, pp[a] | ((pp[a + 1] - pp[a]) << 16), sh);
     }

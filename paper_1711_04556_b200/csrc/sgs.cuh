@@ -78,12 +78,12 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 template <int W>
 __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
-                                           uint32_t hi, int esv, int dur, int sh, int* err) {
+                                           uint32_t hi, int esv, int dur, uint32_t dmask,
+                                           int* err) {
   const int lane = threadIdx.x & 31;
   // lane i tests the window [t0+i, t0+i+dur) inside the round: a candidate
   // iff it ends in the round, a hit iff dur fitting slots start at bit i
   const bool cand = lane + dur <= 32;
-  const uint32_t dmask = dur >= 32 ? 0xffffffffu : (1u << dur) - 1u;
   int t0 = esv, carry = 0;
   for (;;) {
     const int t = t0 + lane;
@@ -170,7 +170,8 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
   int start = esv;
   if (dur > 0 && (r0 | r1) != 0) {
     if (esv < hw)
-      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur, rec.w, err);
+      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                static_cast<uint32_t>(rec.w), err);
     warp_commit<W>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
@@ -270,7 +271,7 @@ __device__ __forceinline__ int sgs_time_split(uint32_t a_info, uint32_t a_push, 
     bool scanning = need && esv < hw;
     int start = esv;
     if (__any_sync(FULL_MASK, scanning)) {
-      const int sh = rec.w;
+      const int sh = window_shifts(dur);
       int t0 = esv, carry = 0;
       do {
         const int t = t0 + lg;

@@ -180,6 +180,15 @@ def pick_group(n: int) -> int:
     return 32
 
 
+def pick_cap_group(n: int, m: int, rmax: int) -> int:
+    """CAPACITY evaluator for the search kernel (measured on B200,
+    profiles/r1/configs): one thread per schedule while its per-thread state
+    (m*rmax + rmax + n words) is small -- j30/j60/j120: 1.45x/1.5x/1.07x the
+    warp evaluator -- else one warp per schedule (300 activities, capacity 80:
+    the per-thread state leaves too few lanes resident)."""
+    return 1 if m * rmax + rmax + n <= 256 else 32
+
+
 # ---------------------------------------------------------------------------
 # single-purpose batches (the operator layer and the parity tests use these)
 
@@ -255,7 +264,12 @@ def run_chunk_batch(inst: ProjectInstance, mode: int, delta: int, orders, tabu_l
     mbuf = torch.zeros((S, nb), dtype=torch.int32, device="cuda")
     cbuf = torch.zeros((S, nb), dtype=torch.int32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    g = pick_group(n) if group is None else group
+    if group is not None:
+        g = group
+    elif mode == MODE_CAPACITY:
+        g = pick_cap_group(n, len(inst.capacities), max(int(c) for c in inst.capacities))
+    else:
+        g = pick_group(n)
     check(L.rcpsp_run_chunk_batch(ptr(di.blob), int(mode), int(delta), T, S, ptr(d_ord),
                                   ptr(d_tabu), ptr(d_head), *(ptr(v) for v in vecs),
                                   int(floor_cmax), ptr(best), ptr(trace), tcap, ptr(stats),
@@ -389,7 +403,7 @@ class SolveConfig:
     threads: int = 0          # 0 = auto (two CTAs per SM when they fit)
     steal: bool = True        # B > 1: idle workers help instances with budget left
     full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluators
-    cap_group: int = 32       # CAPACITY: 32 = one warp per schedule, 1 = one thread
+    cap_group: int | None = None  # CAPACITY: 32 = warp, 1 = thread per schedule, None = auto
 
     @property
     def block_iters(self) -> int:
@@ -535,7 +549,8 @@ class BatchSolver:
         mode, words = group_key if group_key is not None else (MODE_TIME, 1)
         a.words = words
         if mode == MODE_CAPACITY:
-            a.group = cfg.cap_group
+            a.group = cfg.cap_group if cfg.cap_group is not None else pick_cap_group(
+                self.n_max, self.m_max, self.rmax_max)
         else:
             a.group = cfg.group if cfg.group is not None else pick_group(self.n_max)
         a.threads = cfg.threads
