@@ -50,6 +50,22 @@ __device__ __forceinline__ int4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// predicated forms: straight-line code instead of a (potentially divergent)
+// branch with a reconvergence point around it
+__device__ __forceinline__ uint32_t lds32_if(bool p, uint32_t a, uint32_t dflt) {
+  uint32_t v = dflt;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q ld.shared.u32 %0, [%2];\n\t}"
+               : "+r"(v) : "r"(static_cast<uint32_t>(p)), "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u32 [%1], %2;\n\t}"
+               ::"r"(static_cast<uint32_t>(p)), "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_shared_if(bool p, uint32_t a, int v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.max.s32 [%1], %2;\n\t}"
+               ::"r"(static_cast<uint32_t>(p)), "r"(a), "r"(v) : "memory");
+}
 // es[s] = max(es[s], v) as one shared-memory reduction (no return value)
 __device__ __forceinline__ void red_max_shared(uint32_t a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -121,11 +137,11 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
       if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
     }
   const int t = start + lane;  // one slot per lane (a loop only for dur > 32)
-  if (lane < dur) {
+  {
     const uint32_t adr = a_tau + 4 * W * t;
-    const bool old = t < hw;
-    sts32(adr, (old ? lds32(adr) : cap0) - r0);
-    if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
+    const bool in = lane < dur, old = in && t < hw;
+    sts32_if(in, adr, lds32_if(old, adr, cap0) - r0);
+    if (W == 2) sts32_if(in, adr + 4, lds32_if(old, adr + 4, cap1) - r1);
   }
   if (dur > 32)
     for (int tt = t + 32; tt < fin; tt += 32) {
@@ -177,13 +193,15 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
   const int fin = start + dur;
   cmax = max(cmax, fin);
   const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-  if (lane < ecnt)  // push the finish time to the successors' es
-    red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + lane)), fin);
+  {  // push the finish time to the successors' es
+    const bool pe = lane < ecnt;
+    red_max_shared_if(pe, a_es + 4 * lds32_if(pe, a_push + 4 * (e0 + lane), 0u), fin);
+  }
   if (ecnt > 32)
     for (int e = lane + 32; e < ecnt; e += 32)
       red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
   if (starts_out && lane == 0) starts_out[act] = start;
-  if (REC && lane == 0) sts32(a_es + 4 * act, static_cast<uint32_t>(start));
+  if (REC) sts32_if(lane == 0, a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
   return start;
 }
@@ -520,7 +538,7 @@ __device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t
     const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
     if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
   }
-  if (REC && lane == 0) sts32(a_es + 4 * act, static_cast<uint32_t>(start));
+  if (REC) sts32_if(lane == 0, a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
   return start;
 }
