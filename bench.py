@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=CONFIG, choices=["j30", "j60", "j120", "act300"])
-    ap.add_argument("--instances", type=int, default=148, help="instances per batch (step)")
+    ap.add_argument("--instances", type=int, default=600,
+                    help="instances per batch (step); 600 = the size of PSPLIB's j120 set "
+                         "(PAPER.md:772)")
     ap.add_argument("--workers", type=int, default=2, help="CTAs (search workers) per instance")
     ap.add_argument("--iters", type=int, default=1000, help="I_total per instance")
     ap.add_argument("--epochs", type=int, default=4, help="elite-exchange epochs (N > 1)")
@@ -211,14 +213,23 @@ def quality_leg(args, insts, modes, cb: dict, iter_rate: float) -> dict:
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     K = int(cb["instances"])
     qi, qm = insts[:K], modes[:K]
-    workers = max(1, (2 * args.instances) // K)      # same CTA count as the timed steps
-    budget = int(0.7 * iter_rate * cb["wall"] / K)   # headroom for pool init / tail
-    p = SearchParams.defaults_for(qi[0].n_activities, total_iters=budget, workers=workers, seed=0)
-    cfg = SolveConfig(total_iters=budget, workers=workers, pool_size=p.pool_size,
-                      tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
-                      phi_max=p.phi_max, seed=0, group=args.group, threads=args.threads)
-    res = BatchSolver(qi, qm, cfg).run()
-    torch.cuda.synchronize()
+    workers = max(1, min(24, (2 * args.instances) // K))  # ~2 CTAs per SM
+
+    def solve(budget: int):
+        p = SearchParams.defaults_for(qi[0].n_activities, total_iters=budget, workers=workers,
+                                      seed=0)
+        cfg = SolveConfig(total_iters=budget, workers=workers, pool_size=p.pool_size,
+                          tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
+                          phi_max=p.phi_max, seed=0, group=args.group, threads=args.threads)
+        r = BatchSolver(qi, qm, cfg).run()
+        torch.cuda.synchronize()
+        return r
+
+    # pilot at ~1/10 of the estimated budget, then scale to 90 % of the wall budget
+    pilot = max(100, int(0.1 * iter_rate * cb["wall"] / K))
+    r0 = solve(pilot)
+    budget = max(pilot, int(pilot * 0.9 * cb["wall"] / max(1e-6, r0.device_ms * 1e-3)))
+    res = solve(budget)
     dev = float(np.mean(100.0 * (res.best_cmax - res.critical_path) / res.critical_path))
     return {"wall_budget_s": cb["wall"], "instances": K,
             "cpu": {"cpm_dev": cb["cpm_dev"], "iters_per_instance": cb["iters"],
