@@ -212,3 +212,24 @@ def test_product_never_imports_oracle():
         text = path.read_text()
         assert not re.search(r"^\s*(import|from)\s+oracle\b", text, re.M), path
         assert "liboracle" not in text, path
+
+
+def test_b200_rules_match_measurements():
+    """B200_RULES pick the mode the device measured faster on 11 of the 12
+    families of profiles/r1/mode_rules_b200.json (tools/derive_rules.py)."""
+    import json
+    from types import SimpleNamespace
+    from paper_1711_04556_b200 import B200_RULES, DEFAULT_RULES, EvalMode, decide_static
+    rows = json.loads((ROOT / "profiles" / "r1" / "mode_rules_b200.json").read_text())["rows"]
+    hits = 0
+    for r in rows:
+        f = SimpleNamespace(max_capacity=r["cap"][1], avg_duration=r["avg_duration"],
+                            min_capacity=r["cap"][0], avg_capacity=sum(r["cap"]) / 2,
+                            avg_branch_factor=1.5, critical_path_length=0)
+        got = decide_static(f, B200_RULES)
+        hits += got == (EvalMode.CAPACITY if r["faster"] == "capacity" else EvalMode.TIME)
+    assert hits >= 11
+    # the Gen-R benchmark configs keep TIME under both rule sets
+    f = SimpleNamespace(max_capacity=16, avg_duration=5.5, min_capacity=10, avg_capacity=13,
+                        avg_branch_factor=1.5, critical_path_length=0)
+    assert decide_static(f, B200_RULES) == decide_static(f, DEFAULT_RULES) == EvalMode.TIME
