@@ -518,6 +518,92 @@ __device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_ev
   }
 }
 
+// CAP, one thread per schedule, reusing the current schedule's prefix.  A
+// warp takes L consecutive moves at once (lane l: move base + l); moves are
+// dealt in increasing index order, so lane 0 has the smallest u of the batch,
+// u_min, and the warp keeps one shared prefix state for positions < u_min
+// (extended with the known starts `bst`, whole warp per resource row).  Every
+// lane copies it into its own state and schedules positions u_min.. of its
+// swapped order; positions u_min..u-1 are the current order's, booked at their
+// known starts.
+//   per-warp scratch: L lanes x (c [m*R] | cb [R] | es [n]) interleaved by lane
+//                     | c_pre [m*rs] | cb_w [rs] | es_pre [n]
+__device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_base, int o_bst,
+                                                       int o_ctr, int o_evs,
+                                                       const uint32_t* __restrict__ moves,
+                                                       int* __restrict__ cmax_out, int n_feas,
+                                                       int warp_words, int lanes) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = I.n, m = I.m, R = I.rmax, rs = cap_row_stride(R), L = lanes;
+  const int* base = dsm + o_base;
+  const int* bst = dsm + o_bst;
+  int* st = dsm + o_evs + warp * warp_words;
+  int* cpre = st + L * cap_thread_words(n, m, R);
+  int* esp = cpre + (m + 1) * rs;
+  const uint32_t a_cpre = sa(cpre), a_cbw = sa(cpre + m * rs), a_dem = sa(I.dem),
+                 a_ctr = sa(dsm + o_ctr);
+  const int capk = lane < m ? I.cap[lane] : 0;
+  int* c = st + lane;                     // c[(k*R + i)*L]
+  int* cb = st + (m * R) * L + lane;      // cb[i*L]
+  int* es = cb + R * L;                   // es[a*L]
+  for (int j = lane; j < m * rs; j += 32) cpre[j] = 0;
+  for (int a = lane; a < n; a += 32) esp[a] = 0;
+  __syncwarp();
+  // batch size: all warps busy on small neighbourhoods (j30: ~90 moves)
+  const int nw = blockDim.x >> 5;
+  const int bsz = min(L, max(1, (n_feas + nw - 1) / nw));
+  int up = 0, cm_pre = 0, steps = 0;
+  for (;;) {
+    int b0 = 0;
+    if (lane == 0) b0 = atomicAdd(reinterpret_cast<int*>(dsm + o_ctr), bsz);
+    b0 = __shfl_sync(FULL_MASK, b0, 0);
+    if (b0 >= n_feas) break;
+    const int idx = b0 + lane;
+    const bool active = lane < bsz && idx < n_feas;
+    const uint32_t mv = moves[active ? idx : b0];
+    const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    const int u0 = __shfl_sync(FULL_MASK, u, 0);
+    // ---- extend the shared prefix to positions < u0 (known starts)
+    for (; up < u0; ++up) {
+      const int act = base[up];
+      const int dur = I.dur[act], s0 = bst[act];
+      if (dur > 0) {
+        const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
+        cap_commit_all(a_cpre, a_cbw, rs, m, capk, req, s0, dur);
+      }
+      const int fin = s0 + dur;
+      cm_pre = max(cm_pre, fin);
+      for (int e = I.sptr[act] + lane; e < I.sptr[act + 1]; e += 32) atomicMax(&esp[I.sdat[e]], fin);
+      __syncwarp();
+    }
+    if (active) {
+      for (int k = 0; k < m; ++k)
+        for (int i = 0; i < R; ++i) c[(k * R + i) * L] = cpre[k * rs + i];
+      for (int a = 0; a < n; ++a) es[a * L] = esp[a];
+      const int au = base[v], av = base[u];
+      int cm = cm_pre;
+      for (int p = u0; p < n; ++p) {
+        const int act = p == u ? au : (p == v ? av : base[p]);
+        const int dur = I.dur[act];
+        const int* dem = I.dem + act * m;
+        const int start = p < u ? bst[act] : max(es[act * L], cap_es(c, L, dem, I.cap, m, R));
+        cap_commit(c, cb, L, dem, I.cap, m, R, start, dur);
+        const int fin = start + dur;
+        cm = max(cm, fin);
+        for (int e = I.sptr[act]; e < I.sptr[act + 1]; ++e) {
+          const int sc = I.sdat[e];
+          if (es[sc * L] < fin) es[sc * L] = fin;
+        }
+      }
+      cmax_out[idx] = cm;
+      steps += n - u0;
+    }
+    __syncwarp();
+  }
+  steps = __reduce_add_sync(FULL_MASK, steps);
+  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
+}
+
 // every compacted move -> cmax_buf (full SGS of the swapped order)
 template <int MODE, int G, int W>
 __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
@@ -571,8 +657,29 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
                         c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
                         c.warp_words, c.inc);
   } else {
-    eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
-                   c.warp_words, c.cap_lanes);
+    // prefix reuse pays from j60 on; on j30-size projects the per-batch state
+    // copy and the current-schedule pass outweigh the shorter suffixes
+    // (131.9 M vs 163 M schedules/s on j30, 147.4 M vs 123 M on j60)
+    if (c.inc && c.I.n >= 48) {
+      // the current order's schedule (starts -> bst) on warp 0's prefix scratch
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (warp == 0) {
+        int* scr = c.evs + c.cap_lanes * cap_thread_words(c.I.n, c.I.m, c.I.rmax);
+        sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
+                     cap_row_stride(c.I.rmax), sa(scr), sa(c.base), c.bst);
+        if (lane == 0) {
+          c.scal[SC_CTR] = 0;
+          c.scal[SC_STEPS] = c.I.n;
+        }
+      }
+      __syncthreads();
+      eval_moves_cap_thread_inc(c.I, soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
+                                soff(c.evs), c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
+                                c.cap_lanes);
+    } else {
+      eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
+                     c.warp_words, c.cap_lanes);
+    }
   }
   __syncthreads();
 }
@@ -629,8 +736,9 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     }
     cta_eval_moves<MODE, G, W>(c, n_feas);
     evals += n_feas;
-    steps += (G == 32 && (MODE == MODE_CAPACITY || c.inc))
-                 ? c.scal[SC_STEPS] : static_cast<long long>(n_feas) * n;
+    const bool counted =
+        MODE == MODE_CAPACITY ? (G == 32 || (c.inc && n >= 48)) : (G == 32 && c.inc);
+    steps += counted ? c.scal[SC_STEPS] : static_cast<long long>(n_feas) * n;
     const int asp = best_known_cmax < local_best ? best_known_cmax : local_best;
     unsigned ka = 0xffffffffu, kl = 0xffffffffu;
     for (int idx = tid; idx < n_feas; idx += blockDim.x) {
@@ -729,7 +837,7 @@ __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, in
                                                int rmax, int cap_lanes) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
-  return cap_lanes * cap_thread_words(n, m, rmax);
+  return cap_lanes * cap_thread_words(n, m, rmax) + cap_warp_words(n, m, rmax);
 }
 
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,

@@ -381,11 +381,11 @@ def test_full_sgs_equals_prefix_reuse():
     insts = synth.benchmark_batch("j120", 4, first_seed=7)
     modes = [1, 0, 1, 0]
     out = []
-    for full, cap_group in ((False, 32), (True, 32), (False, 1)):
+    for full, cap_group in ((False, 32), (True, 32), (False, 1), (True, 1)):
         cfg = SolveConfig(total_iters=120, workers=1, pool_size=8, tabu_size=800, delta=60,
                           phi_steps=20, phi_max=3, seed=1, collect_trace=True, full_sgs=full,
                           cap_group=cap_group)
         r = BatchSolver(insts, modes, cfg).run()
         out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
                     [[t.tolist() for t in tr] for tr in r.traces]))
-    assert out[0] == out[1] == out[2]
+    assert out[0] == out[1] == out[2] == out[3]
