@@ -92,6 +92,18 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 // Each round tests 32 slots and resolves the window branch-free: the run
 // carried from the previous round, else the first run of `dur` ones.
 template <int W>
+__device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
+                                                       uint32_t r0, uint32_t r1, uint32_t cap0,
+                                                       uint32_t cap1, uint32_t hi) {
+  uint32_t w0 = cap0, w1 = cap1;
+  if (t < hw) {
+    w0 = lds32(a_tau + 4 * W * t);
+    if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
+  }
+  return __ballot_sync(FULL_MASK, t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi)));
+}
+
+template <int W>
 __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
                                            uint32_t hi, int esv, int dur, uint32_t dmask,
@@ -100,26 +112,24 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   // lane i tests the window [t0+i, t0+i+dur) inside the round: a candidate
   // iff it ends in the round, a hit iff dur fitting slots start at bit i
   const bool cand = lane + dur <= 32;
-  int t0 = esv, carry = 0;
+  // first round, peeled: nothing is carried in, so lane 0's test covers the
+  // window starting at esv
+  uint32_t m = window_fits_ballot<W>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
+  uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
+  if (y) return esv + __ffs(y) - 1;
+  int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
   for (;;) {
-    const int t = t0 + lane;
-    uint32_t w0 = cap0, w1 = cap1;
-    if (t < hw) {
-      w0 = lds32(a_tau + 4 * W * t);
-      if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
-    }
-    const bool ok = t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi));
-    const uint32_t m = __ballot_sync(FULL_MASK, ok);
-    const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
-    if (carry + tz >= dur) return t0 - carry;
-    const uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
-    if (y) return t0 + __ffs(y) - 1;
-    carry = tz == 32 ? carry + 32 : __clz(~m);
     t0 += 32;
     if (t0 >= H) {  // cannot happen for valid instances
       if (lane == 0) set_err(err, DE_NO_WINDOW);
       return H;
     }
+    m = window_fits_ballot<W>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
+    const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
+    if (carry + tz >= dur) return t0 - carry;
+    y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
+    if (y) return t0 + __ffs(y) - 1;
+    carry = tz == 32 ? carry + 32 : __clz(~m);
   }
 }
 
