@@ -348,36 +348,57 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     __syncwarp();
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
-    // after scheduling `act` at position p: log bookings below hw_pre for the
-    // undo; true once the state provably equals the current schedule's
-    auto after = [&](int act, int st) -> bool {
+    // log the bookings below hw_pre for the undo
+    auto log_below = [&](int act, int st) {
       if (st < hw_pre) {
         if (lane == 0) sts32(a_log + 4 * nlog, static_cast<uint32_t>(act));
         ++nlog;
       }
-      if (!div) {
-        div = st != static_cast<int>(lds32(a_bst + 4 * act));
-        if (!div && p >= v) return true;
-      }
-      return false;
     };
-    // unrolled by two so the prefetched next activity needs no register copies
-    int act_a = static_cast<int>(lds32(a_ord + 4 * u));
-    int4 rec_a = lds128(a_info + 16 * act_a);
+    // phase A, positions u..v: until a start differs from the current
+    // schedule's (then phase B) or v is reached with none differing
+    // (converged: the rest is the current schedule)
+    int act = static_cast<int>(lds32(a_ord + 4 * u));
+    int4 rec = lds128(a_info + 16 * act);
     for (;;) {
-      const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
-      const int4 rec_b = lds128(a_info + 16 * act_b);
-      int st = time_step_warp<W, true>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
-                                       a_es, hw, cm, nullptr, err);
-      if (after(act_a, st) || ++p >= n) break;
-      act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
-      rec_a = lds128(a_info + 16 * act_a);
-      st = time_step_warp<W, true>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
-                                   hw, cm, nullptr, err);
-      if (after(act_b, st) || ++p >= n) break;
+      const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
+      const int4 rec_n = lds128(a_info + 16 * act_n);
+      const int st = time_step_warp<W, true>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
+                                             a_es, hw, cm, nullptr, err);
+      log_below(act, st);
+      div = st != static_cast<int>(lds32(a_bst + 4 * act));
+      if (div || p == v) {
+        ++p;
+        act = act_n;
+        rec = rec_n;
+        break;
+      }
+      ++p;
+      act = act_n;
+      rec = rec_n;
+    }
+    // phase B, positions p..n-1 after a divergence; unrolled by two so the
+    // prefetched next activity needs no register copies
+    if (div) {
+      int act_a = act;
+      int4 rec_a = rec;
+      for (;;) {
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+        const int4 rec_b = lds128(a_info + 16 * act_b);
+        int st = time_step_warp<W, true>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
+                                         a_es, hw, cm, nullptr, err);
+        log_below(act_a, st);
+        if (++p >= n) break;
+        act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+        rec_a = lds128(a_info + 16 * act_a);
+        st = time_step_warp<W, true>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
+                                     hw, cm, nullptr, err);
+        log_below(act_b, st);
+        if (++p >= n) break;
+      }
     }
     if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
-    steps += (p < n ? p + 1 : n) - u;
+    steps += p - u;  // converged: p = v + 1; else n
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     for (int k = 0; k < nlog; ++k) {
