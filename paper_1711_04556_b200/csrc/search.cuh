@@ -349,9 +349,10 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
     // log the bookings below hw_pre for the undo
+    // (entry: start << 16 | activity; horizons are < 2^16, see KEY_LIMIT)
     auto log_below = [&](int act, int st) {
       if (st < hw_pre) {
-        if (lane == 0) sts32(a_log + 4 * nlog, static_cast<uint32_t>(act));
+        if (lane == 0) sts32(a_log + 4 * nlog, (static_cast<uint32_t>(st) << 16) | act);
         ++nlog;
       }
     };
@@ -363,7 +364,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (;;) {
       const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
       const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_warp<W, true>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
+      const int st = time_step_warp<W, false>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                              a_es, hw, cm, nullptr, err);
       log_below(act, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
@@ -385,13 +386,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_warp<W, true>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
+        int st = time_step_warp<W, false>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                          a_es, hw, cm, nullptr, err);
         log_below(act_a, st);
         if (++p >= n) break;
         act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_warp<W, true>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
+        st = time_step_warp<W, false>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
                                      hw, cm, nullptr, err);
         log_below(act_b, st);
         if (++p >= n) break;
@@ -402,12 +403,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     for (int k = 0; k < nlog; ++k) {
-      const int a = static_cast<int>(lds32(a_log + 4 * k));
+      const uint32_t ent = lds32(a_log + 4 * k);
+      const int a = static_cast<int>(ent & 0xffffu);
       const int4 r = lds128(a_info + 16 * a);
       const uint32_t r0 = static_cast<uint32_t>(r.y);
       const uint32_t r1 = W == 2 ? lds32(a_req + 8 * a + 4) : 0u;
       if (r.x > 0 && (r0 | r1) != 0) {
-        warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(lds32(a_es + 4 * a)), r.x, r0, r1);
+        warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(ent >> 16), r.x, r0, r1);
       }
     }
     __syncwarp();
