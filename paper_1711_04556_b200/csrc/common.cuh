@@ -18,7 +18,7 @@ enum { MODE_CAPACITY = 0, MODE_TIME = 1 };  // kernels.py:22-23
 
 enum BlobField {
   B_MAGIC = 0, B_N = 1, B_M = 2, B_H = 3, B_E = 4, B_W = 5, B_LB = 6, B_RMAX = 7, B_CPM = 8,
-  B_LEN = 9, B_NLVL = 10,
+  B_LEN = 9, B_NLVL = 10, B_BIG = 11,
   B_OFF_DUR = 16, B_OFF_DEM = 17, B_OFF_CAP = 18, B_OFF_PPTR = 19, B_OFF_PDAT = 20,
   B_OFF_SPTR = 21, B_OFF_SDAT = 22, B_OFF_REQ = 23, B_OFF_CAPW = 24, B_OFF_LPTR = 25,
   B_OFF_LDAT = 26,
@@ -46,6 +46,7 @@ __device__ __forceinline__ void set_err(int* err, int code) {
 //       window test looks for (the split evaluators derive window_shifts).
 struct SInst {
   int n, m, H, e, W, rmax, cpm;
+  int big;               // a duration or fan-out > 32 (multi-round paths needed)
   uint32_t hi;           // high bit of every packed resource lane (TIME fits test)
   const int4* info_f;    // [n] forward records
   const int4* info_r;    // [n] reversed-project records
@@ -94,6 +95,7 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
   I.W = blob[B_W];
   I.rmax = blob[B_RMAX];
   I.cpm = blob[B_CPM];
+  I.big = blob[B_BIG];
   I.hi = blob[B_LB] == 8 ? 0x80808080u : 0x80008000u;
   const int n = I.n, m = I.m, e = I.e, W = I.W;
   int4* inf = reinterpret_cast<int4*>(smem);  // smem base is 16-byte aligned

@@ -301,7 +301,7 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 //   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n] | log [n] | ord [n]
 // The log lists the suffix activities booked below hw_pre (the only ones the
 // undo has to visit).
-template <int W>
+template <int W, bool BIG>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
                                                    uint32_t cap1, uint32_t hi, int n, int H,
@@ -331,7 +331,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       const int s = static_cast<int>(lds32(a_bst + 4 * act));
       const uint32_t r0 = static_cast<uint32_t>(rec.y);
       const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
-      if (rec.x > 0 && (r0 | r1) != 0) warp_commit<W>(a_tau, hw_pre, s, rec.x, r0, r1, cap0, cap1);
+      if (rec.x > 0 && (r0 | r1) != 0) warp_commit<W, BIG>(a_tau, hw_pre, s, rec.x, r0, r1, cap0, cap1);
       const int fin = s + rec.x;
       cm_pre = max(cm_pre, fin);
       const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
@@ -364,7 +364,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (;;) {
       const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
       const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_warp<W, false>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
+      const int st = time_step_warp<W, false, BIG>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                              a_es, hw, cm, nullptr, err);
       log_below(act, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
@@ -386,13 +386,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_warp<W, false>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
+        int st = time_step_warp<W, false, BIG>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                          a_es, hw, cm, nullptr, err);
         log_below(act_a, st);
         if (++p >= n) break;
         act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_warp<W, false>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
+        st = time_step_warp<W, false, BIG>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
                                      hw, cm, nullptr, err);
         log_below(act_b, st);
         if (++p >= n) break;
@@ -648,10 +648,18 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
           }
         }
         __syncthreads();
-        eval_moves_time32_inc<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
-                                 soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0],
-                                 W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, c.moves_buf,
-                                 c.cmax_buf, n_feas, c.warp_words, c.scal[SC_BASEC], c.err);
+        if (c.I.big)
+          eval_moves_time32_inc<W, true>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req),
+                                         soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
+                                         soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
+                                         c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
+                                         c.warp_words, c.scal[SC_BASEC], c.err);
+        else
+          eval_moves_time32_inc<W, false>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req),
+                                          soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
+                                          soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
+                                          c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
+                                          c.warp_words, c.scal[SC_BASEC], c.err);
       } else {
         eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
                              soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,

@@ -135,7 +135,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
 
 // Book an activity on [start, start+dur) (kernels.py:139-146): materialise
 // [hw, start) at capacity, subtract the packed demand, advance hw.
-template <int W>
+template <int W, bool BIG = true>
 __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, int dur,
                                             uint32_t r0, uint32_t r1, uint32_t cap0,
                                             uint32_t cap1) {
@@ -153,7 +153,7 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
     sts32_if(in, adr, lds32_if(old, adr, cap0) - r0);
     if (W == 2) sts32_if(in, adr + 4, lds32_if(old, adr + 4, cap1) - r1);
   }
-  if (dur > 32)
+  if (BIG && dur > 32)
     for (int tt = t + 32; tt < fin; tt += 32) {
       const uint32_t adr = a_tau + 4 * W * tt;
       const bool old = tt < hw;
@@ -182,7 +182,8 @@ __device__ __forceinline__ void warp_uncommit(uint32_t a_tau, int hw_keep, int s
 // One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
 // Returns the start; REC also records it in es[act] (dead once the activity
 // is scheduled), where the prefix-reusing evaluator's undo finds it.
-template <int W, bool REC = false>
+// BIG = false: the instance has no duration and no fan-out above 32 (I.big).
+template <int W, bool REC = false, bool BIG = true>
 __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t a_push,
                                                uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                                uint32_t hi, int H, uint32_t a_tau,
@@ -198,7 +199,7 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
     if (esv < hw)
       start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
                                 static_cast<uint32_t>(rec.w), err);
-    warp_commit<W>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
+    warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
   cmax = max(cmax, fin);
@@ -207,7 +208,7 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
     const bool pe = lane < ecnt;
     red_max_shared_if(pe, a_es + 4 * lds32_if(pe, a_push + 4 * (e0 + lane), 0u), fin);
   }
-  if (ecnt > 32)
+  if (BIG && ecnt > 32)
     for (int e = lane + 32; e < ecnt; e += 32)
       red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
   if (starts_out && lane == 0) starts_out[act] = start;

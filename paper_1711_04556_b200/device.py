@@ -27,7 +27,7 @@ MODE_CAPACITY = 0
 MODE_TIME = 1
 BLOB_MAGIC = 0x52435053
 HDR = 32
-(B_MAGIC, B_N, B_M, B_H, B_E, B_W, B_LB, B_RMAX, B_CPM, B_LEN, B_NLVL) = range(11)
+(B_MAGIC, B_N, B_M, B_H, B_E, B_W, B_LB, B_RMAX, B_CPM, B_LEN, B_NLVL, B_BIG) = range(12)
 (B_OFF_DUR, B_OFF_DEM, B_OFF_CAP, B_OFF_PPTR, B_OFF_PDAT, B_OFF_SPTR, B_OFF_SDAT, B_OFF_REQ,
  B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT) = range(16, 27)
 
@@ -106,6 +106,10 @@ def pack_instance(inst: ProjectInstance) -> np.ndarray:
     hdr[B_CPM] = critical_path_length(inst)
     hdr[B_LEN] = off
     hdr[B_NLVL] = len(levels)
+    # 1 when a duration or a fan-out exceeds one warp (32): the forward search
+    # evaluator's multi-round booking / push paths are compiled out otherwise
+    fan = max([len(x) for x in inst.successors] + [0])
+    hdr[B_BIG] = int(max(int(d) for d in inst.durations) > 32 or fan > 32)
     return np.concatenate([hdr] + [np.asarray(p, np.int32) for p in parts])
 
 
