@@ -2,10 +2,12 @@
 """Benchmark: evaluated schedules/sec of the B200 tabu search (BASELINE.json).
 
 One "step" = one full on-device solve of a batch of synthetic j120-shape
-instances (Gen-R, the reference's own benchmark recipe): pool
+instances: by default "Gen-P", 600 PSPLIB-shape instances over PSPLIB j120's
+(NC, RF, RS) parameter grid (synth.progen_instance; PSPLIB itself is offline),
+or "Gen-R", the reference's own benchmark recipe (--config j120).  Pool
 initialisation (FBI), then the persistent search with the working set in HBM,
-per-instance evaluation mode picked by the paper's static rules (TIME for this
-config).  value = evaluated schedules (the reference's counting rule: pool +
+per-instance evaluation mode picked by the paper's static rules (TIME for
+these configs).  value = evaluated schedules (the reference's counting rule: pool +
 per-adoption + every neighbourhood evaluation) / device time of the step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -37,7 +39,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG = "j120"
+CONFIG = "j120p"
 METRIC = "evaluated schedules/sec at 1/2/4/8 B200, j120-shape; mean % dev from CPM bound"
 
 
@@ -47,7 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=CONFIG, choices=["j30", "j60", "j120", "act300"])
+    ap.add_argument("--config", default=CONFIG,
+                    choices=["j30", "j60", "j120", "act300", "j30p", "j60p", "j120p"],
+                    help="Gen-R (reference benchmark recipe) or Gen-P (*p: PSPLIB grid)")
     ap.add_argument("--instances", type=int, default=600,
                     help="instances per batch (step); 600 = the size of PSPLIB's j120 set "
                          "(PAPER.md:772)")
@@ -140,19 +144,35 @@ def work_per_schedule(cfg: str) -> dict:
 # ---------------------------------------------------------------------------
 # reference arm / cpu baseline (the C port of the reference, oracle/)
 
-def cpu_sample(cfg: str, iters: int, target_s: float, threads: int, seed: int = 0) -> dict:
+def workload_name(cfg: str) -> str:
+    if cfg.endswith("p"):
+        return (f"{cfg[:-1]}-shape Gen-P batch (PSPLIB {cfg[:-1]} NC/RF/RS grid, "
+                f"ProGen-style synthetic)")
+    return f"{cfg}-shape Gen-R batch (reference benchmark recipe)"
+
+
+SAMPLE_STRIDE = 157  # coprime with the batch sizes used: the sample spreads over the batch
+
+
+def sample_index(k: int, batch: int) -> int:
+    """Batch index of the k-th CPU-sample instance (spread over Gen-P's grid cells)."""
+    return (k * SAMPLE_STRIDE) % batch
+
+
+def cpu_sample(cfg: str, iters: int, target_s: float, threads: int, batch: int,
+               seed: int = 0) -> dict:
     """Time the reference algorithm (C port, `threads` workers per instance,
     instances one after another like `rcpsp-tabu bench`) on a bounded sample
-    of the workload.  Returns schedules/sec, the sample and the CPM deviation."""
+    of the workload: instances sample_index(0..) of the step's batch.  Returns
+    schedules/sec, the sample and the CPM deviation."""
     import oracle
     from paper_1711_04556_b200 import extract_features, decide_static, synth
     evals = 0
     wall = 0.0
     devs = []
     k = 0
-    first_seed = 0
     while True:
-        inst = synth.benchmark_batch(cfg, 1, first_seed=first_seed + k)[0]
+        inst = synth.benchmark_batch(cfg, 1, first_seed=sample_index(k, batch))[0]
         mode = int(decide_static(extract_features(inst)))
         r = oracle.orchestrate(inst, iters, threads, seed, mode)
         evals += r["evaluations"]
@@ -173,16 +193,17 @@ def run_reference(args, ws: int, rank: int) -> None:
     iters = args.iters
     per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(args.config, min(iters, 50), 0.5, cores)
+        cpu_sample(args.config, min(iters, 50), 0.5, cores, args.instances)
     vals, evals, walls, devs = [], 0, 0.0, []
     for _ in range(args.steps):
-        r = cpu_sample(args.config, iters, per_step, cores)
+        r = cpu_sample(args.config, iters, per_step, cores, args.instances)
         vals.append(r["value"])
         evals += r["evaluations"]
         walls += r["wall"]
         devs.append(r["cpm_dev"])
     value = evals / walls
-    sample = (f"{args.config} Gen-R seeds 0..{r['instances'] - 1}, I_total={iters}, "
+    sample = (f"{r['instances']} {args.config} instances of the {args.instances}-instance batch "
+              f"(indices k*{SAMPLE_STRIDE} mod {args.instances}), I_total={iters}, "
               f"{cores} worker threads per instance, instances solved one after another "
               f"(~{per_step:.0f} s per step)")
     line = {
@@ -190,7 +211,7 @@ def run_reference(args, ws: int, rank: int) -> None:
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * walls / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-shape Gen-R batch, reference C port on host",
+        "config": {"workload": f"{workload_name(args.config)}, reference C port on host",
                    "iters_per_instance": iters, "cpm_dev": float(np.mean(devs))},
         "cpu_baseline": {"value": value, "unit": "schedules/s", "cores": cores, "kind": "port",
                          "sample": sample},
@@ -212,7 +233,8 @@ def quality_leg(args, insts, modes, cb: dict, iter_rate: float) -> dict:
     from paper_1711_04556_b200 import SearchParams
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     K = int(cb["instances"])
-    qi, qm = insts[:K], modes[:K]
+    pick = [sample_index(k, len(insts)) for k in range(K)]  # the CPU sample's instances
+    qi, qm = [insts[i] for i in pick], [modes[i] for i in pick]
     workers = max(1, min(24, (2 * args.instances) // K))  # ~2 CTAs per SM
 
     def solve(budget: int):
@@ -402,8 +424,8 @@ def main() -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}-shape Gen-R batch (reference benchmark recipe), "
-                               f"static-rule mode selection", "instances": I,
+        "config": {"workload": f"{workload_name(args.config)}, static-rule mode selection",
+                   "instances": I,
                    "workers_per_instance": args.workers, "iters_per_instance": args.iters,
                    "pool_size": p.pool_size, "delta": p.delta, "tabu_size": p.tabu_size,
                    "modes": {"TIME": modes.count(1), "CAPACITY": modes.count(0)},
@@ -430,10 +452,11 @@ def main() -> None:
     if ws == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.cpu_count()
-        cb = cpu_sample(args.config, args.iters, args.cpu_seconds, cores)
+        cb = cpu_sample(args.config, args.iters, args.cpu_seconds, cores, args.instances)
         line["cpu_baseline"] = {
             "value": cb["value"], "unit": "schedules/s", "cores": cores, "kind": "port",
-            "sample": f"{cb['instances']} {args.config} Gen-R instances (seeds 0..), "
+            "sample": f"{cb['instances']} {args.config} instances of the batch "
+                      f"(indices k*{SAMPLE_STRIDE} mod {args.instances}), "
                       f"I_total={cb['iters']}, {cores} worker threads each, "
                       f"{cb['wall']:.1f} s; cpm_dev {cb['cpm_dev']:.2f}%"}
         if not args.no_quality:
