@@ -57,7 +57,9 @@ def parse():
                          "(PAPER.md:772)")
     ap.add_argument("--workers", type=int, default=2, help="CTAs (search workers) per instance")
     ap.add_argument("--iters", type=int, default=1000, help="I_total per instance")
-    ap.add_argument("--epochs", type=int, default=4, help="elite-exchange epochs (N > 1)")
+    ap.add_argument("--epochs", type=int, default=2,
+                    help="search epochs with an elite exchange between them (N > 1); every "
+                         "epoch boundary drains the GPU once")
     ap.add_argument("--group", type=int, default=None, help="TIME lanes per schedule")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
     ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
