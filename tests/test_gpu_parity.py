@@ -188,6 +188,47 @@ def test_neighbourhood_makespans_shapes():
         _check_neighbourhood(inst, orders, 0, delta, int(rng.choice(CAP_GROUPS)), (seed, "cap"))
 
 
+def _edge_instances():
+    """Shapes the prefix-reusing evaluators must survive: zero durations, one
+    unit of one resource (fully serial), demand == capacity everywhere, a hub
+    with 40 successors (fan-out > 32 -> the multi-round push path), durations
+    above 32 (multi-round booking / windows), no resource use at all."""
+    from paper_1711_04556_b200 import make_instance
+    rng = np.random.default_rng(31)
+    out = []
+    # zero durations sprinkled in, single resource of capacity 1
+    n = 24
+    durs = [0] + [int(x) if rng.random() < 0.7 else 0 for x in rng.integers(1, 6, n - 2)] + [0]
+    succ = [[1, 2, 3]] + [[min(n - 1, i + 1 + int(rng.integers(0, 3)))] for i in range(1, n - 1)] + [[]]
+    out.append(make_instance("serial1", durs, [1], [[0]] + [[1]] * (n - 2) + [[0]], succ))
+    # demand == capacity for every used resource
+    dem = [[0, 0]] + [[3, 0] if i % 2 else [0, 5] for i in range(1, n - 1)] + [[0, 0]]
+    out.append(make_instance("full", [0] + [int(x) for x in rng.integers(1, 8, n - 2)] + [0],
+                             [3, 5], dem, succ))
+    # hub: activity 1 precedes 40 activities
+    n = 46
+    succ = ([[1]] + [list(range(2, 42))] + [[42 + (i % 3)] for i in range(2, 42)]
+            + [[n - 1] for _ in range(42, n - 1)] + [[]])
+    dem = [[0, 0]] + [[int(x) for x in rng.integers(0, 6, 2)] for _ in range(n - 2)] + [[0, 0]]
+    out.append(make_instance("hub40", [0] + [int(x) for x in rng.integers(1, 9, n - 2)] + [0],
+                             [6, 7], dem, succ))
+    # long durations (> 32)
+    out.append(synth.random_instance(30, 3, seed=77, cap_lo=4, cap_hi=9, max_dur=70,
+                                     demand_density=0.8))
+    # no resource demand at all (the SGS is the critical-path schedule)
+    out.append(synth.random_instance(25, 2, seed=78, demand_density=0.0))
+    return out
+
+
+def test_neighbourhood_makespans_edge_shapes():
+    rng = np.random.default_rng(37)
+    for inst in _edge_instances():
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(4)])
+        for mode, group in ((1, 32), (1, 16), (0, 32), (0, 1)):
+            _check_neighbourhood(inst, orders, mode, inst.n_activities, group,
+                                 (inst.name, mode, group))
+
+
 def test_run_chunk_batch_independent(ginst):
     """Several searches in one launch give the same results as one each."""
     inst = ginst["genr60s0"]
