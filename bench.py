@@ -445,7 +445,9 @@ def main() -> None:
                      "sgs_steps_per_schedule": sgs_steps / max(1, search_evals),
                      "executed_step_fraction": sgs_steps / max(1, search_evals * n_act),
                      "peak_source": "measured in this run: rcpsp_smem_probe (LDS.128 stream)",
-                     "hbm_peak_gbs": hbm_peak},
+                     "hbm_peak_gbs": hbm_peak,
+                     "hbm_achieved_gbs": (traffic * args.steps * epochs / (s_ms * 1e-3) / 1e9
+                                          if traffic is not None else None)},
         "clocks": clk,
         "gpu_launches": launches,
         "e2e": {"value": e2e, "unit": "schedules/s", "h2d_bytes_per_step": h2d,
