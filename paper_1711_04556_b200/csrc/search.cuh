@@ -22,7 +22,7 @@ namespace rt {
 enum Scal {
   SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
   SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_BASEC,
-  SC_CTR, SC_STEPS, SC_WORDS = 32
+  SC_CTR, SC_STEPS, SC_BSTOK, SC_WORDS = 32
 };
 
 struct CtaCtx {
@@ -271,6 +271,11 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
   }
 }
 
+// cmax_buf entries of moves whose schedule converged to the current one carry
+// this flag (makespans are < 2^16): when such a move is picked, the next
+// iteration's current schedule has the same starts and needs no new pass
+constexpr int CONV_FLAG = 1 << 30;
+
 __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
   int old;
   asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(a) : "memory");
@@ -398,7 +403,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
         if (++p >= n) break;
       }
     }
-    if (lane == 0) cmax_out[idx] = div ? cm : base_cmax;
+    if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);
     steps += p - u;  // converged: p = v + 1; else n
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
@@ -636,15 +641,19 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
         // the current order's schedule (starts -> bst), then prefix-reusing moves
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         if (warp == 0) {
-          uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
-          int* es = c.evs + (c.I.H + 1) * W;
-          const int cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req), c.I.capw[0],
-                                          W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H,
-                                          sa(tau), sa(es), sa(c.base), c.bst, c.err);
+          const bool keep = c.scal[SC_BSTOK] != 0;  // picked move had converged
+          if (!keep) {
+            uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
+            int* es = c.evs + (c.I.H + 1) * W;
+            const int cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req),
+                                            c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+                                            c.I.n, c.I.H, sa(tau), sa(es), sa(c.base), c.bst,
+                                            c.err);
+            if (lane == 0) c.scal[SC_BASEC] = cm;
+          }
           if (lane == 0) {
-            c.scal[SC_BASEC] = cm;
             c.scal[SC_CTR] = 0;
-            c.scal[SC_STEPS] = c.I.n;  // the current order's schedule
+            c.scal[SC_STEPS] = keep ? 0 : c.I.n;  // the current order's schedule
           }
         }
         __syncthreads();
@@ -758,6 +767,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
   const int tid = threadIdx.x, n = c.I.n;
   int local_best = start_cmax, cur = start_cmax, iters = 0, forced = 0;
   long long evals = 0, steps = 0;
+  if (tid == 0) c.scal[SC_BSTOK] = 0;  // a new order: no current-schedule starts yet
   for (int it = 0; it < budget; ++it) {
     const int n_feas = cta_filter(c);
     ++iters;
@@ -773,7 +783,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     const int asp = best_known_cmax < local_best ? best_known_cmax : local_best;
     unsigned ka = 0xffffffffu, kl = 0xffffffffu;
     for (int idx = tid; idx < n_feas; idx += blockDim.x) {
-      const unsigned cm = static_cast<unsigned>(c.cmax_buf[idx]);
+      const unsigned cm = static_cast<unsigned>(c.cmax_buf[idx]) & 0xffffu;
       const unsigned key = (cm << 16) | static_cast<unsigned>(idx);
       kl = min(kl, key);
       const uint32_t mv = c.moves_buf[idx];
@@ -795,6 +805,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
       c.base[v] = t;
       c.scal[SC_HEAD] = tabu_add1(c, c.scal[SC_HEAD], u, v);
       if (trace) trace[iters - 1] = cur;
+      c.scal[SC_BSTOK] = (c.cmax_buf[pick] & CONV_FLAG) ? 1 : 0;
     }
     __syncthreads();
     if (cur < local_best) {

@@ -285,7 +285,7 @@ def run_chunk_batch(inst: ProjectInstance, mode: int, delta: int, orders, tabu_l
     # the last iteration's compacted neighbourhood and its makespans
     n_last = st[:, 1] if int(budget.max()) == 1 else None
     mv = mbuf.cpu().numpy().view(np.uint32)
-    cm = cbuf.cpu().numpy()
+    cm = cbuf.cpu().numpy() & 0xFFFF   # high bits: evaluator flags (CONV_FLAG)
     last = None
     if n_last is not None:
         last = [(np.stack([(mv[b, :k] >> 16).astype(np.int32),
