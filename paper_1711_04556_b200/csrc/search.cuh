@@ -322,6 +322,11 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
   __syncwarp();
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
+  // the last position holds the sink (every activity precedes it, and moves
+  // never reach it): with zero duration it starts at max(es) <= cm, so it
+  // cannot change the makespan and is not scheduled
+  const int pend = lds128(a_info + 16 * static_cast<int>(lds32(a_base + 4 * (n - 1)))).x == 0
+                       ? n - 1 : n;
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = atom_inc_shared(a_ctr);
@@ -383,9 +388,9 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       act = act_n;
       rec = rec_n;
     }
-    // phase B, positions p..n-1 after a divergence; unrolled by two so the
+    // phase B, positions p..pend-1 after a divergence; unrolled by two so the
     // prefetched next activity needs no register copies
-    if (div) {
+    if (div && p < pend) {
       int act_a = act;
       int4 rec_a = rec;
       for (;;) {
@@ -394,17 +399,17 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
         int st = time_step_warp<W, false, BIG>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
                                          a_es, hw, cm, nullptr, err);
         log_below(act_a, st);
-        if (++p >= n) break;
+        if (++p >= pend) break;
         act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_warp<W, false, BIG>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
                                      hw, cm, nullptr, err);
         log_below(act_b, st);
-        if (++p >= n) break;
+        if (++p >= pend) break;
       }
     }
     if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);
-    steps += p - u;  // converged: p = v + 1; else n
+    steps += p - u;  // converged: p = v + 1; else pend
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     for (int k = 0; k < nlog; ++k) {
