@@ -303,7 +303,7 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | es [n] | es_pre [n] | log [n] | ord [n]
+//   per-warp scratch: tau (H+1)*W | fin [n] | log [n] | ord [n]
 // The log lists the suffix activities booked below hw_pre (the only ones the
 // undo has to visit).
 template <int W, bool BIG>
@@ -315,12 +315,12 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                                                    int warp_words, int base_cmax, int* err) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* ws = dsm + o_evs + warp * warp_words;
-  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_req = sa(dsm + o_req),
+  // o_info: pull records (info_r: duration, demand, predecessor span, mask);
+  // o_pull: predecessor lists (pdat)
+  const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
-                 a_tau = sa(ws), a_es = sa(ws + (H + 1) * W), a_esp = a_es + 4 * n,
-                 a_log = a_esp + 4 * n, a_ord = a_log + 4 * n;
-  for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
-  __syncwarp();
+                 a_tau = sa(ws), a_fin = sa(ws + (H + 1) * W), a_log = a_fin + 4 * n,
+                 a_ord = a_log + 4 * n;
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
   // the last position holds the sink (every activity precedes it, and moves
   // never reach it): with zero duration it starts at max(es) <= cm, so it
@@ -344,17 +344,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       if (rec.x > 0 && (r0 | r1) != 0) warp_commit<W, BIG>(a_tau, hw_pre, s, rec.x, r0, r1, cap0, cap1);
       const int fin = s + rec.x;
       cm_pre = max(cm_pre, fin);
-      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-      for (int e = lane; e < ecnt; e += 32) {
-        const uint32_t adr = a_esp + 4 * lds32(a_push + 4 * (e0 + e));
-        if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-      }
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
       __syncwarp();
     }
-    // ---- the swapped order's suffix u.. (materialised), es from the prefix
+    // ---- the swapped order's suffix u.. (materialised); fin of the prefix
+    // activities holds their current finish times, the suffix overwrites its
+    // own entries before any successor pulls them
     for (int q = u + lane; q < n; q += 32)
       sts32(a_ord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
-    for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
     __syncwarp();
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
@@ -374,8 +371,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (;;) {
       const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
       const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_warp<W, false, BIG>(act, rec, a_push, a_req, cap0, cap1, hi, H, a_tau,
-                                             a_es, hw, cm, nullptr, err);
+      const int st = time_step_pull<W, BIG>(act, rec, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
+                                            a_fin, hw, cm, err);
       log_below(act, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
       if (div || p == v) {
@@ -396,14 +393,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_warp<W, false, BIG>(act_a, rec_a, a_push, a_req, cap0, cap1, hi, H, a_tau,
-                                         a_es, hw, cm, nullptr, err);
+        int st = time_step_pull<W, BIG>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
+                                          a_tau, a_fin, hw, cm, err);
         log_below(act_a, st);
         if (++p >= pend) break;
         act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_warp<W, false, BIG>(act_b, rec_b, a_push, a_req, cap0, cap1, hi, H, a_tau, a_es,
-                                     hw, cm, nullptr, err);
+        st = time_step_pull<W, BIG>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
+                                      a_fin, hw, cm, err);
         log_below(act_b, st);
         if (++p >= pend) break;
       }
@@ -663,13 +660,13 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
         }
         __syncthreads();
         if (c.I.big)
-          eval_moves_time32_inc<W, true>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req),
+          eval_moves_time32_inc<W, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
                                          soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
                                          soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
                                          c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
                                          c.warp_words, c.scal[SC_BASEC], c.err);
         else
-          eval_moves_time32_inc<W, false>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req),
+          eval_moves_time32_inc<W, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
                                           soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
                                           soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
                                           c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
@@ -882,7 +879,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n : (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 3 * n : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return cap_lanes * cap_thread_words(n, m, rmax) + cap_warp_words(n, m, rmax);
 }

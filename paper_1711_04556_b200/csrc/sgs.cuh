@@ -217,6 +217,40 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
   return start;
 }
 
+// One activity with pulled precedence: es = max over the predecessors of
+// fin[pred] (kernels.py:177-182 computes es_prec exactly so), then the window
+// and the booking as time_step_warp; fin[act] is recorded.  rec is the
+// activity's pull record (info_r: duration, demand, predecessor span, mask).
+template <int W, bool BIG>
+__device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t a_pdat,
+                                              uint32_t a_req, uint32_t cap0, uint32_t cap1,
+                                              uint32_t hi, int H, uint32_t a_tau, uint32_t a_fin,
+                                              int& hw, int& cmax, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
+  const bool pl = lane < pc;
+  int f = static_cast<int>(lds32_if(pl, a_fin + 4 * lds32_if(pl, a_pdat + 4 * (p0 + lane), 0u), 0u));
+  if (BIG && pc > 32)
+    for (int e = lane + 32; e < pc; e += 32)
+      f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
+  const int esv = __reduce_max_sync(FULL_MASK, f);
+  const int dur = rec.x;
+  const uint32_t r0 = static_cast<uint32_t>(rec.y);
+  const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
+  int start = esv;
+  if (dur > 0 && (r0 | r1) != 0) {
+    if (esv < hw)
+      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                             static_cast<uint32_t>(rec.w), err);
+    warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
+  }
+  const int fin = start + dur;
+  cmax = max(cmax, fin);
+  sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
+  __syncwarp();
+  return start;
+}
+
 // Warp-uniform time-indexed SGS (G = 32, one schedule per warp).  Same
 // results as the reference's time-indexed SGS; every branch is warp-uniform
 // and every shared access goes through a precomputed 32-bit shared address.

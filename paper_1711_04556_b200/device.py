@@ -106,9 +106,14 @@ def pack_instance(inst: ProjectInstance) -> np.ndarray:
     hdr[B_CPM] = critical_path_length(inst)
     hdr[B_LEN] = off
     hdr[B_NLVL] = len(levels)
-    # 1 when a duration or a fan-out exceeds one warp (32): the forward search
-    # evaluator's multi-round booking / push paths are compiled out otherwise
-    fan = max([len(x) for x in inst.successors] + [0])
+    # 1 when a duration, a fan-out or a fan-in exceeds one warp (32): the
+    # search evaluator's multi-round booking / pull paths are compiled out
+    # otherwise.  The zero-duration sink (last activity) is never scheduled by
+    # it, so its fan-in does not count.
+    sink_free = int(inst.durations[n - 1]) == 0
+    fan = max([len(x) for x in inst.successors]
+              + [len(x) for i, x in enumerate(inst.predecessors)
+                 if not (sink_free and i == n - 1)] + [0])
     hdr[B_BIG] = int(max(int(d) for d in inst.durations) > 32 or fan > 32)
     return np.concatenate([hdr] + [np.asarray(p, np.int32) for p in parts])
 
