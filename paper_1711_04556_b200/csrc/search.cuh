@@ -287,11 +287,13 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // For the swap (u, v) (u < v) the swapped order equals the current one on
 // positions < u, so the serial SGS state after those positions is the
 // current schedule's.  Each warp keeps that prefix state -- profile below
-// the mark hw_pre, es pushed by the prefix (es_pre), its makespan -- and
-// extends it with the known starts `bst` as its u grows: moves are handed
-// out in increasing (lexicographic) index order by a shared counter, so a
-// warp's u never decreases.  A move then schedules positions u.. only, and
-// undoes its bookings below hw_pre afterwards.
+// the mark hw_pre, the finish times of the prefix activities, its makespan --
+// and extends it with the known starts `bst` as its u grows: moves are
+// handed out in increasing (lexicographic) index order by a shared counter,
+// so a warp's u never decreases.  A move then schedules positions u.. only
+// (precedence pulled: es = max over the predecessors' finish times, which
+// the suffix overwrites for its own activities before any successor reads
+// them), and undoes its bookings below hw_pre afterwards.
 //
 // Convergence: the SGS state after position p is a function of the starts
 // of the activities at positions <= p.  If every activity at positions
@@ -304,8 +306,8 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
 //   per-warp scratch: tau (H+1)*W | fin [n] | log [n] | ord [n]
-// The log lists the suffix activities booked below hw_pre (the only ones the
-// undo has to visit).
+// The log lists the suffix activities booked below hw_pre with their starts
+// (the only bookings the undo has to give back).
 template <int W, bool BIG>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,

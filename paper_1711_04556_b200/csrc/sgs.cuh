@@ -179,11 +179,10 @@ __device__ __forceinline__ void warp_uncommit(uint32_t a_tau, int hw_keep, int s
   }
 }
 
-// One activity of the warp-uniform time-indexed SGS (see sgs_time_warp).
-// Returns the start; REC also records it in es[act] (dead once the activity
-// is scheduled), where the prefix-reusing evaluator's undo finds it.
+// One activity of the warp-uniform time-indexed SGS (see sgs_time_warp), push
+// form: the finish time goes to the successors' es.  Returns the start.
 // BIG = false: the instance has no duration and no fan-out above 32 (I.big).
-template <int W, bool REC = false, bool BIG = true>
+template <int W, bool BIG = true>
 __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t a_push,
                                                uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                                uint32_t hi, int H, uint32_t a_tau,
@@ -212,7 +211,6 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
     for (int e = lane + 32; e < ecnt; e += 32)
       red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
   if (starts_out && lane == 0) starts_out[act] = start;
-  if (REC) sts32_if(lane == 0, a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
   return start;
 }
@@ -583,7 +581,6 @@ __device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t
     const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
     if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
   }
-  if (REC) sts32_if(lane == 0, a_es + 4 * act, static_cast<uint32_t>(start));
   __syncwarp();
   return start;
 }
