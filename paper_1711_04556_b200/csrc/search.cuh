@@ -305,9 +305,10 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | fin [n] | log [n] | ord [n]
-// The log lists the suffix activities booked below hw_pre with their starts
-// (the only bookings the undo has to give back).
+//   per-warp scratch: tau (H+1)*W | fin [n] | log [2n] | ord [n]
+// The log lists the suffix bookings below hw_pre -- (start | dur << 16,
+// packed demand (W = 1) or activity (W = 2)) -- the only ones the undo has to
+// give back (a zero demand gives back nothing).
 template <int W, bool BIG>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
@@ -321,8 +322,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   // o_pull: predecessor lists (pdat)
   const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
-                 a_tau = sa(ws), a_fin = sa(ws + (H + 1) * W), a_log = a_fin + 4 * n,
-                 a_ord = a_log + 4 * n;
+                 a_tau = sa(ws), a_fin = sa(ws + (H + 1) * W),
+                 a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + 8 * n;
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
   // the last position holds the sink (every activity precedes it, and moves
   // never reach it): with zero duration it starts at max(es) <= cm, so it
@@ -359,9 +360,10 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     bool div = false;
     // log the bookings below hw_pre for the undo
     // (entry: start << 16 | activity; horizons are < 2^16, see KEY_LIMIT)
-    auto log_below = [&](int act, int st) {
-      if (st < hw_pre) {
-        if (lane == 0) sts32(a_log + 4 * nlog, (static_cast<uint32_t>(st) << 16) | act);
+    auto log_below = [&](int act, const int4& rec, int st) {
+      if (st < hw_pre && rec.x > 0) {
+        if (lane == 0) sts64(a_log + 8 * nlog, (static_cast<uint32_t>(rec.x) << 16) | st,
+                             W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act));
         ++nlog;
       }
     };
@@ -375,7 +377,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       const int4 rec_n = lds128(a_info + 16 * act_n);
       const int st = time_step_pull<W, BIG>(act, rec, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
                                             a_fin, hw, cm, err);
-      log_below(act, st);
+      log_below(act, rec, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
       if (div || p == v) {
         ++p;
@@ -397,13 +399,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
                                           a_tau, a_fin, hw, cm, err);
-        log_below(act_a, st);
+        log_below(act_a, rec_a, st);
         if (++p >= pend) break;
         act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_pull<W, BIG>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
                                       a_fin, hw, cm, err);
-        log_below(act_b, st);
+        log_below(act_b, rec_b, st);
         if (++p >= pend) break;
       }
     }
@@ -412,14 +414,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     for (int k = 0; k < nlog; ++k) {
-      const uint32_t ent = lds32(a_log + 4 * k);
-      const int a = static_cast<int>(ent & 0xffffu);
-      const int4 r = lds128(a_info + 16 * a);
-      const uint32_t r0 = static_cast<uint32_t>(r.y);
-      const uint32_t r1 = W == 2 ? lds32(a_req + 8 * a + 4) : 0u;
-      if (r.x > 0 && (r0 | r1) != 0) {
-        warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(ent >> 16), r.x, r0, r1);
+      const uint2 ent = lds64(a_log + 8 * k);
+      uint32_t r0 = ent.y, r1 = 0u;
+      if (W == 2) {
+        r0 = lds32(a_req + 8 * ent.y);
+        r1 = lds32(a_req + 8 * ent.y + 4);
       }
+      warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(ent.x & 0xffffu),
+                       static_cast<int>(ent.x >> 16), r0, r1);
     }
     __syncwarp();
   }
@@ -881,7 +883,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 3 * n : (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n + 2 : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return cap_lanes * cap_thread_words(n, m, rmax) + cap_warp_words(n, m, rmax);
 }

@@ -66,6 +66,14 @@ __device__ __forceinline__ void red_max_shared_if(bool p, uint32_t a, int v) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.max.s32 [%1], %2;\n\t}"
                ::"r"(static_cast<uint32_t>(p)), "r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
 // es[s] = max(es[s], v) as one shared-memory reduction (no return value)
 __device__ __forceinline__ void red_max_shared(uint32_t a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
