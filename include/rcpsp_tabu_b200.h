@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 3
+#define RCPSP_ABI_VERSION 4
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -83,6 +83,11 @@ typedef struct RcpspSolveArgs {
     int64_t full_sgs;           /* 1 = evaluate every swap by a full SGS;
                                  * 0 (default) = group 32 reuses the base
                                  * order's schedule prefix (same makespans) */
+    int64_t cluster;            /* CTAs per worker (thread-block cluster,
+                                 * 1..8): the leader CTA runs the search, the
+                                 * others evaluate neighbourhood moves over
+                                 * distributed shared memory (TIME group 32
+                                 * only; others run with 1) */
 } RcpspSolveArgs;
 
 int rcpsp_abi_version(void);

@@ -522,16 +522,30 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
                                                   int n_ids, SmemPlan plan) {
   int* smem = dsm;
   const int B = static_cast<int>(A.workers);
-  const int slot0 = blockIdx.x / B, wk = blockIdx.x % B;
+  // with clusters (A.cluster > 1, TIME group 32 only) a worker is a cluster
+  // of CTAs: rank 0 runs the search, the others only evaluate moves
+  const int C = A.cluster > 1 ? static_cast<int>(A.cluster) : 1;
+  const int wkr = blockIdx.x / C;  // worker index in the launch
+  const int slot0 = wkr / B, wk = wkr % B;
   int slot = slot0;
   int iid = ids[slot];
   const int tid = threadIdx.x;
   const int F = static_cast<int>(A.pool_size), T = static_cast<int>(A.tabu_size);
   CtaCtx c;
   cta_setup(c, A.blob + A.blob_off[iid], smem, plan, static_cast<int>(A.delta), T,
-            A.moves_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max,
-            A.cmax_buf + static_cast<size_t>(blockIdx.x) * A.nbhd_max, A.err);
+            A.moves_buf + static_cast<size_t>(wkr) * A.nbhd_max,
+            A.cmax_buf + static_cast<size_t>(wkr) * A.nbhd_max, A.err);
   c.inc = A.full_sgs == 0;
+  if constexpr (MODE == MODE_TIME && G == 32) {
+    if (C > 1) {
+      if (cluster_rank() != 0) {
+        cta_follow<W>(c, A, iid, smem, plan.inst);
+        return;
+      }
+      c.csize = C;
+      if (tid == 0) c.scal[SC_IID] = iid;
+    }
+  }
   const size_t wid = static_cast<size_t>(iid) * B + wk;  // this worker's rng / stats slot
   int64_t* st = A.w_stats + wid * 16;
   int* wtrace = A.collect_trace ? A.w_trace + wid * A.trace_cap : nullptr;
@@ -645,6 +659,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
       Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
       __syncthreads();
       stage_instance(A.blob + A.blob_off[iid], smem + plan.inst, c.I);
+      if (tid == 0) c.scal[SC_IID] = iid;
       __syncthreads();
       cta_init_rows(c);
       continue;
@@ -696,6 +711,12 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
       ++chunks;
       tlen += o.iters;
     }
+  }
+  if (c.csize > 1) {  // release the followers, then keep this CTA alive until they are out
+    if (tid == 0) c.scal[SC_CMD] = CMD_DONE;
+    __syncthreads();
+    cluster_sync_all();
+    cluster_sync_all();
   }
   if (tid == 0) {
     st[WK_CHUNKS] = chunks;
@@ -1028,8 +1049,29 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
-    const int grid = n_ids * static_cast<int>(A.workers);
-    k<<<grid, nt, p.total * 4, s>>>(A, inst_ids, n_ids, p);
+    int C = (MODE == MODE_TIME && G == 32 && A.full_sgs == 0) ? static_cast<int>(A.cluster) : 1;
+    if (C < 1) C = 1;
+    if (C > 8) return fail("cluster must be 1..8 CTAs");
+    A.cluster = C;
+    const int grid = n_ids * static_cast<int>(A.workers) * C;
+    if (C == 1) {
+      k<<<grid, nt, p.total * 4, s>>>(A, inst_ids, n_ids, p);
+      return launch_check("k_solve");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = p.total * 4;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cuda_check(cudaLaunchKernelEx(&cfg, k, A, inst_ids, n_ids, p), "k_solve (cluster)"))
+      return -1;
     return launch_check("k_solve");
   });
 }

@@ -22,7 +22,7 @@ namespace rt {
 enum Scal {
   SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
   SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_BASEC,
-  SC_CTR, SC_STEPS, SC_BSTOK, SC_WORDS = 32
+  SC_CTR, SC_STEPS, SC_BSTOK, SC_CMD, SC_NF, SC_IID, SC_WORDS = 32
 };
 
 struct CtaCtx {
@@ -44,6 +44,7 @@ struct CtaCtx {
   int warp_words;  // evaluation scratch words per warp
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
   bool inc;        // TIME G = 32: reuse the current order's schedule prefix
+  int csize;       // CTAs of this worker's cluster (1: no cluster); this CTA is the leader
   uint32_t* moves_buf;  // global [nbhd] compacted moves
   int* cmax_buf;        // global [nbhd] makespans
   int* err;
@@ -282,6 +283,35 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
   return old;
 }
 
+// ---- thread-block clusters: distributed shared memory of the leader (rank 0)
+enum ClusterCmd { CMD_EVAL = 1, CMD_DONE = 2 };
+
+__device__ __forceinline__ uint32_t cluster_map(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cluster(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int atom_add_cluster(uint32_t a, int v) {
+  int old;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+// all threads of all CTAs of the cluster; release/acquire at cluster scope
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // TIME, one warp per schedule, reusing the current order's schedule.
 //
 // For the swap (u, v) (u < v) the swapped order equals the current one on
@@ -309,13 +339,16 @@ __device__ __forceinline__ int atom_inc_shared(uint32_t a) {
 // The log lists the suffix bookings below hw_pre -- (start | dur << 16,
 // packed demand (W = 1) or activity (W = 2)) -- the only ones the undo has to
 // give back (a zero demand gives back nothing).
+//   ctr_cl: != 0 -> the move counter (and the step counter after it) live in
+//   the cluster leader's shared memory at this shared::cluster address
 template <int W, bool BIG>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
                                                    uint32_t cap1, uint32_t hi, int n, int H,
                                                    const uint32_t* __restrict__ moves,
                                                    int* __restrict__ cmax_out, int n_feas,
-                                                   int warp_words, int base_cmax, int* err) {
+                                                   int warp_words, int base_cmax, int* err,
+                                                   uint32_t ctr_cl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* ws = dsm + o_evs + warp * warp_words;
   // o_info: pull records (info_r: duration, demand, predecessor span, mask);
@@ -332,7 +365,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                        ? n - 1 : n;
   for (;;) {
     int idx = 0;
-    if (lane == 0) idx = atom_inc_shared(a_ctr);
+    if (lane == 0) idx = ctr_cl ? atom_add_cluster(ctr_cl, 1) : atom_inc_shared(a_ctr);
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_feas) break;
     const uint32_t mv = moves[idx];
@@ -426,7 +459,12 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     __syncwarp();
   }
   // SGS activity steps of this warp: suffixes + prefix extension
-  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
+  if (lane == 0) {
+    if (ctr_cl)
+      atom_add_cluster(ctr_cl + 4, steps + up);
+    else
+      atomicAdd(&dsm[o_ctr + 1], steps + up);
+  }
 }
 
 // TIME, G = 16 / 8 lanes per schedule (S = 32/G schedules per warp)
@@ -638,6 +676,57 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
   if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
 }
 
+// the prefix-reusing TIME evaluator on this CTA's copy of the current order
+template <int W>
+__device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int n_feas,
+                                                           int base_cmax, uint32_t ctr_cl) {
+  if (c.I.big)
+    eval_moves_time32_inc<W, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
+                                   soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
+                                   c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H,
+                                   c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax,
+                                   c.err, ctr_cl);
+  else
+    eval_moves_time32_inc<W, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
+                                    soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
+                                    soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+                                    c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
+                                    base_cmax, c.err, ctr_cl);
+}
+
+// Cluster follower (rank > 0): evaluates moves of the leader's neighbourhood
+// phases until the leader is done.  Per phase: B1 (leader published the
+// phase), copy the current order and its starts from the leader's shared
+// memory, deal moves from the leader's counter, write makespans into the
+// leader's global buffer, B2.  The instance follows the leader's (steals).
+template <int W>
+__device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* smem, int plan_inst) {
+  const int tid = threadIdx.x;
+  const uint32_t l_scal = cluster_map(sa(c.scal), 0);
+  const uint32_t l_base = cluster_map(sa(c.base), 0), l_bst = cluster_map(sa(c.bst), 0);
+  for (;;) {
+    cluster_sync_all();  // B1
+    const int cmd = static_cast<int>(ld_cluster(l_scal + 4 * SC_CMD));
+    if (cmd == CMD_DONE) break;
+    const int liid = static_cast<int>(ld_cluster(l_scal + 4 * SC_IID));
+    if (liid != iid) {
+      iid = liid;
+      stage_instance(A.blob + A.blob_off[iid], smem + plan_inst, c.I);
+    }
+    const int n_feas = static_cast<int>(ld_cluster(l_scal + 4 * SC_NF));
+    const int base_cmax = static_cast<int>(ld_cluster(l_scal + 4 * SC_BASEC));
+    for (int p = tid; p < c.I.n; p += blockDim.x) {
+      c.base[p] = static_cast<int>(ld_cluster(l_base + 4 * p));
+      c.bst[p] = static_cast<int>(ld_cluster(l_bst + 4 * p));
+    }
+    __syncthreads();
+    eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, l_scal + 4 * SC_CTR);
+    __syncthreads();
+    cluster_sync_all();  // B2
+  }
+  cluster_sync_all();  // the leader's shared memory stays valid until every follower is out
+}
+
 // every compacted move -> cmax_buf (full SGS of the swapped order)
 template <int MODE, int G, int W>
 __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
@@ -663,18 +752,20 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
           }
         }
         __syncthreads();
-        if (c.I.big)
-          eval_moves_time32_inc<W, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
-                                         soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
-                                         soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
-                                         c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
-                                         c.warp_words, c.scal[SC_BASEC], c.err);
-        else
-          eval_moves_time32_inc<W, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
-                                          soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
-                                          soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u,
-                                          c.I.hi, c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas,
-                                          c.warp_words, c.scal[SC_BASEC], c.err);
+        if (c.csize > 1) {  // hand the phase to the cluster's other CTAs
+          if (threadIdx.x == 0) {
+            c.scal[SC_NF] = n_feas;
+            c.scal[SC_CMD] = CMD_EVAL;
+          }
+          __syncthreads();
+          cluster_sync_all();  // B1: followers read the leader's state
+        }
+        eval_moves_time32_dispatch<W>(c, n_feas, c.scal[SC_BASEC],
+                                      c.csize > 1 ? cluster_map(sa(c.scal + SC_CTR), 0) : 0u);
+        if (c.csize > 1) {
+          __syncthreads();
+          cluster_sync_all();  // B2: every move of the phase is evaluated
+        }
       } else {
         eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
                              soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
@@ -929,6 +1020,7 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.rowc = smem + p.rowc;
   c.bst = smem + p.bst;
   c.inc = true;
+  c.csize = 1;
   c.tabu_list = reinterpret_cast<uint32_t*>(smem + p.tabu_list);
   c.tabu_cnt = reinterpret_cast<uint32_t*>(smem + p.tabu_cnt);
   c.red = smem + p.red;

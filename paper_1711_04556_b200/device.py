@@ -189,6 +189,20 @@ def pick_group(n: int) -> int:
     return 32
 
 
+def sm_count() -> int:
+    return int(_torch().cuda.get_device_properties(0).multi_processor_count)
+
+
+def pick_cluster(workers_total: int) -> int:
+    """CTAs per worker: a small launch (a single instance, a few workers)
+    leaves most SMs idle, so each worker becomes a thread-block cluster whose
+    CTAs share its neighbourhood evaluation (up to 8; about two CTAs per SM in
+    total).  Batches that fill the GPU run one CTA per worker."""
+    if workers_total <= 0:
+        return 1
+    return max(1, min(8, (2 * sm_count()) // workers_total))
+
+
 def pick_cap_group(n: int, m: int, rmax: int) -> int:
     """CAPACITY evaluator for the search kernel (measured on B200,
     profiles/r1/configs): one thread per schedule while its per-thread state
@@ -413,6 +427,7 @@ class SolveConfig:
     steal: bool = True        # B > 1: idle workers help instances with budget left
     full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluators
     cap_group: int | None = None  # CAPACITY: 32 = warp, 1 = thread per schedule, None = auto
+    cluster: int | None = None    # CTAs per worker (1..8; TIME group 32), None = auto
 
     @property
     def block_iters(self) -> int:
@@ -565,6 +580,10 @@ class BatchSolver:
         a.threads = cfg.threads
         a.steal = int(cfg.steal and cfg.workers > 1 and not cfg.collect_trace)
         a.full_sgs = int(cfg.full_sgs)
+        n_group = len(self.groups.get(group_key, [])) if group_key is not None else len(
+            self.instances)
+        a.cluster = (cfg.cluster if cfg.cluster is not None
+                     else pick_cluster(n_group * cfg.workers))
         return a
 
     def pool_init(self, stream=None) -> None:

@@ -430,3 +430,25 @@ def test_full_sgs_equals_prefix_reuse():
         out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
                     [[t.tolist() for t in tr] for tr in r.traces]))
     assert out[0] == out[1] == out[2] == out[3]
+
+
+def test_cluster_workers_equal_single_cta():
+    """A worker spread over a thread-block cluster (2..8 CTAs sharing the
+    neighbourhood over distributed shared memory) follows the same trajectory
+    as a single-CTA worker (B = 1, traces compared); the multi-worker launch
+    with steals keeps its budget accounting."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts = synth.benchmark_batch("j120p", 3, first_seed=150) + \
+        synth.benchmark_batch("j60", 1, first_seed=3)
+    out = []
+    for cl in (1, 2, 8):
+        cfg = SolveConfig(total_iters=80, workers=1, pool_size=8, tabu_size=800, delta=60,
+                          phi_steps=20, phi_max=3, seed=2, collect_trace=True, cluster=cl)
+        r = BatchSolver(insts, [1] * 4, cfg).run()
+        out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
+                    [[t.tolist() for t in tr] for tr in r.traces]))
+    assert out[0] == out[1] == out[2]
+    cfg = SolveConfig(total_iters=300, workers=3, pool_size=8, tabu_size=800, delta=60,
+                      phi_steps=20, phi_max=3, seed=2, cluster=4)
+    r = BatchSolver(insts, [1] * 4, cfg).run()
+    assert r.iterations.tolist() == [300] * 4
