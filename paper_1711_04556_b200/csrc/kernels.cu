@@ -536,10 +536,10 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
             A.moves_buf + static_cast<size_t>(wkr) * A.nbhd_max,
             A.cmax_buf + static_cast<size_t>(wkr) * A.nbhd_max, A.err);
   c.inc = A.full_sgs == 0;
-  if constexpr (MODE == MODE_TIME && G == 32) {
+  if constexpr ((MODE == MODE_TIME && G == 32) || MODE == MODE_CAPACITY) {
     if (C > 1) {
       if (cluster_rank() != 0) {
-        cta_follow<W>(c, A, iid, smem, plan.inst);
+        cta_follow<MODE, G, W>(c, A, iid, smem, plan.inst, C);
         return;
       }
       c.csize = C;
@@ -1049,7 +1049,10 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
-    int C = (MODE == MODE_TIME && G == 32 && A.full_sgs == 0) ? static_cast<int>(A.cluster) : 1;
+    // clusters need a move counter to share: the prefix-reusing evaluators
+    // (TIME group 32, CAPACITY group 32, CAPACITY group 1 from 48 activities)
+    const bool shared_counter = MODE == MODE_TIME ? G == 32 : (G == 32 || A.n_max >= 48);
+    int C = (shared_counter && A.full_sgs == 0) ? static_cast<int>(A.cluster) : 1;
     if (C < 1) C = 1;
     if (C > 8) return fail("cluster must be 1..8 CTAs");
     A.cluster = C;

@@ -513,7 +513,7 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
                                                  int n, int m, int rs,
                                                  const uint32_t* __restrict__ moves,
                                                  int* __restrict__ cmax_out, int n_feas,
-                                                 int warp_words, bool reuse) {
+                                                 int warp_words, bool reuse, uint32_t ctr_cl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mr = m * rs;
   const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
@@ -528,7 +528,7 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
   int up = 0, cm_pre = 0, steps = 0;
   for (;;) {
     int idx = 0;
-    if (lane == 0) idx = atom_inc_shared(a_ctr);
+    if (lane == 0) idx = ctr_cl ? atom_add_cluster(ctr_cl, 1) : atom_inc_shared(a_ctr);
     idx = __shfl_sync(FULL_MASK, idx, 0);
     if (idx >= n_feas) break;
     const uint32_t mv = moves[idx];
@@ -568,7 +568,12 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
     if (lane == 0) cmax_out[idx] = cm;
     steps += n - u0;
   }
-  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
+  if (lane == 0) {
+    if (ctr_cl)
+      atom_add_cluster(ctr_cl + 4, steps + up);
+    else
+      atomicAdd(&dsm[o_ctr + 1], steps + up);
+  }
 }
 
 // CAP, one thread per schedule
@@ -604,7 +609,8 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
                                                        int o_ctr, int o_evs,
                                                        const uint32_t* __restrict__ moves,
                                                        int* __restrict__ cmax_out, int n_feas,
-                                                       int warp_words, int lanes) {
+                                                       int warp_words, int lanes,
+                                                       uint32_t ctr_cl, int nw_total) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = I.n, m = I.m, R = I.rmax, rs = cap_row_stride(R), L = lanes;
   const int* base = dsm + o_base;
@@ -622,12 +628,13 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
   for (int a = lane; a < n; a += 32) esp[a] = 0;
   __syncwarp();
   // batch size: all warps busy on small neighbourhoods (j30: ~90 moves)
-  const int nw = blockDim.x >> 5;
+  const int nw = nw_total;  // warps sharing the phase (the cluster's)
   const int bsz = min(L, max(1, (n_feas + nw - 1) / nw));
   int up = 0, cm_pre = 0, steps = 0;
   for (;;) {
     int b0 = 0;
-    if (lane == 0) b0 = atomicAdd(reinterpret_cast<int*>(dsm + o_ctr), bsz);
+    if (lane == 0)
+      b0 = ctr_cl ? atom_add_cluster(ctr_cl, bsz) : atomicAdd(reinterpret_cast<int*>(dsm + o_ctr), bsz);
     b0 = __shfl_sync(FULL_MASK, b0, 0);
     if (b0 >= n_feas) break;
     const int idx = b0 + lane;
@@ -673,7 +680,33 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
     __syncwarp();
   }
   steps = __reduce_add_sync(FULL_MASK, steps);
-  if (lane == 0) atomicAdd(&dsm[o_ctr + 1], steps + up);
+  if (lane == 0) {
+    if (ctr_cl)
+      atom_add_cluster(ctr_cl + 4, steps + up);
+    else
+      atomicAdd(&dsm[o_ctr + 1], steps + up);
+  }
+}
+
+// Leader side of a cluster neighbourhood phase (no-ops without a cluster):
+// publish the phase and meet the followers at B1; B2 once every move is done.
+__device__ __forceinline__ void cluster_phase_begin(CtaCtx& c, int n_feas) {
+  if (c.csize <= 1) return;
+  if (threadIdx.x == 0) {
+    c.scal[SC_NF] = n_feas;
+    c.scal[SC_CMD] = CMD_EVAL;
+  }
+  __syncthreads();
+  cluster_sync_all();  // B1: followers read the leader's state
+}
+__device__ __forceinline__ void cluster_phase_end(const CtaCtx& c) {
+  if (c.csize <= 1) return;
+  __syncthreads();
+  cluster_sync_all();  // B2: every move of the phase is evaluated
+}
+// the move counter the phase deals from: the leader's, as a cluster address
+__device__ __forceinline__ uint32_t cluster_counter(const CtaCtx& c) {
+  return c.csize > 1 ? cluster_map(sa(c.scal + SC_CTR), 0) : 0u;
 }
 
 // the prefix-reusing TIME evaluator on this CTA's copy of the current order
@@ -699,8 +732,9 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
 // phase), copy the current order and its starts from the leader's shared
 // memory, deal moves from the leader's counter, write makespans into the
 // leader's global buffer, B2.  The instance follows the leader's (steals).
-template <int W>
-__device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* smem, int plan_inst) {
+template <int MODE, int G, int W>
+__device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* smem, int plan_inst,
+                           int csize) {
   const int tid = threadIdx.x;
   const uint32_t l_scal = cluster_map(sa(c.scal), 0);
   const uint32_t l_base = cluster_map(sa(c.base), 0), l_bst = cluster_map(sa(c.bst), 0);
@@ -720,7 +754,20 @@ __device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* sme
       c.bst[p] = static_cast<int>(ld_cluster(l_bst + 4 * p));
     }
     __syncthreads();
-    eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, l_scal + 4 * SC_CTR);
+    const uint32_t ctr = l_scal + 4 * SC_CTR;
+    if constexpr (MODE == MODE_TIME) {
+      eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, ctr);
+    } else if constexpr (G == 32) {
+      eval_moves_cap_warp(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.dem), soff(c.I.cap),
+                          soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.n,
+                          c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
+                          c.warp_words, true, ctr);
+    } else {
+      eval_moves_cap_thread_inc(c.I, soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
+                                soff(c.evs), c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
+                                c.cap_lanes, ctr, static_cast<int>(blockDim.x >> 5) * csize);
+    }
+    (void)base_cmax;
     __syncthreads();
     cluster_sync_all();  // B2
   }
@@ -752,20 +799,9 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
           }
         }
         __syncthreads();
-        if (c.csize > 1) {  // hand the phase to the cluster's other CTAs
-          if (threadIdx.x == 0) {
-            c.scal[SC_NF] = n_feas;
-            c.scal[SC_CMD] = CMD_EVAL;
-          }
-          __syncthreads();
-          cluster_sync_all();  // B1: followers read the leader's state
-        }
-        eval_moves_time32_dispatch<W>(c, n_feas, c.scal[SC_BASEC],
-                                      c.csize > 1 ? cluster_map(sa(c.scal + SC_CTR), 0) : 0u);
-        if (c.csize > 1) {
-          __syncthreads();
-          cluster_sync_all();  // B2: every move of the phase is evaluated
-        }
+        cluster_phase_begin(c, n_feas);
+        eval_moves_time32_dispatch<W>(c, n_feas, c.scal[SC_BASEC], cluster_counter(c));
+        cluster_phase_end(c);
       } else {
         eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),
                              soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n,
@@ -789,10 +825,12 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
       }
     }
     __syncthreads();
+    cluster_phase_begin(c, n_feas);
     eval_moves_cap_warp(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.dem), soff(c.I.cap),
                         soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.n,
                         c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
-                        c.warp_words, c.inc);
+                        c.warp_words, c.inc, cluster_counter(c));
+    cluster_phase_end(c);
   } else {
     // prefix reuse pays from j60 on; on j30-size projects the per-batch state
     // copy and the current-schedule pass outweigh the shorter suffixes
@@ -810,9 +848,12 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
         }
       }
       __syncthreads();
+      cluster_phase_begin(c, n_feas);
       eval_moves_cap_thread_inc(c.I, soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
                                 soff(c.evs), c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
-                                c.cap_lanes);
+                                c.cap_lanes, cluster_counter(c),
+                                static_cast<int>(blockDim.x >> 5) * c.csize);
+      cluster_phase_end(c);
     } else {
       eval_moves_cap(c.I, soff(c.base), soff(c.evs), c.moves_buf, c.cmax_buf, n_feas,
                      c.warp_words, c.cap_lanes);

@@ -440,14 +440,16 @@ def test_cluster_workers_equal_single_cta():
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     insts = synth.benchmark_batch("j120p", 3, first_seed=150) + \
         synth.benchmark_batch("j60", 1, first_seed=3)
-    out = []
-    for cl in (1, 2, 8):
-        cfg = SolveConfig(total_iters=80, workers=1, pool_size=8, tabu_size=800, delta=60,
-                          phi_steps=20, phi_max=3, seed=2, collect_trace=True, cluster=cl)
-        r = BatchSolver(insts, [1] * 4, cfg).run()
-        out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
-                    [[t.tolist() for t in tr] for tr in r.traces]))
-    assert out[0] == out[1] == out[2]
+    for modes, cap_group in (([1] * 4, None), ([1, 0, 0, 1], 32), ([0, 1, 0, 0], 1)):
+        out = []
+        for cl in (1, 2, 8):
+            cfg = SolveConfig(total_iters=80, workers=1, pool_size=8, tabu_size=800, delta=60,
+                              phi_steps=20, phi_max=3, seed=2, collect_trace=True, cluster=cl,
+                              cap_group=cap_group)
+            r = BatchSolver(insts, modes, cfg).run()
+            out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
+                        [[t.tolist() for t in tr] for tr in r.traces]))
+        assert out[0] == out[1] == out[2], (modes, cap_group)
     cfg = SolveConfig(total_iters=300, workers=3, pool_size=8, tabu_size=800, delta=60,
                       phi_steps=20, phi_max=3, seed=2, cluster=4)
     r = BatchSolver(insts, [1] * 4, cfg).run()
