@@ -226,40 +226,38 @@ def run_reference(args, ws: int, rank: int) -> None:
 # ---------------------------------------------------------------------------
 # B200 arm
 
-def quality_leg(args, insts, modes, cb: dict, iter_rate: float) -> dict:
+def quality_leg(args, insts, modes, cb: dict) -> dict:
     """Mean % deviation from the CPM bound at a fixed wall-clock budget: the
-    CPU sample's instances (first K seeds) solved on the GPU within the wall
-    time the reference algorithm took for them on all host cores.  The GPU
-    budget per instance is calibrated from the timed steps' iteration rate."""
+    CPU sample's instances solved on the GPU within the wall time the
+    reference algorithm took for them on all host cores.  The search stops on
+    the device clock (SolveConfig.time_limit_s -> %globaltimer): no new grant
+    and no further iteration once the budget is spent."""
     import torch
     from paper_1711_04556_b200 import SearchParams
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     K = int(cb["instances"])
     pick = [sample_index(k, len(insts)) for k in range(K)]  # the CPU sample's instances
     qi, qm = [insts[i] for i in pick], [modes[i] for i in pick]
-    workers = max(1, min(24, (2 * args.instances) // K))  # ~2 CTAs per SM
-
-    def solve(budget: int):
-        p = SearchParams.defaults_for(qi[0].n_activities, total_iters=budget, workers=workers,
-                                      seed=0)
-        cfg = SolveConfig(total_iters=budget, workers=workers, pool_size=p.pool_size,
-                          tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
-                          phi_max=p.phi_max, seed=0, group=args.group, threads=args.threads)
-        r = BatchSolver(qi, qm, cfg).run()
-        torch.cuda.synchronize()
-        return r
-
-    # pilot at ~1/10 of the estimated budget, then scale to 90 % of the wall budget
-    pilot = max(100, int(0.1 * iter_rate * cb["wall"] / K))
-    r0 = solve(pilot)
-    budget = max(pilot, int(pilot * 0.9 * cb["wall"] / max(1e-6, r0.device_ms * 1e-3)))
-    res = solve(budget)
+    # every CTA must be resident from the start (2 per SM): a wave that starts
+    # after the clock stopped the search would never run
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    workers = max(1, (2 * sms) // K)
+    budget_iters = 10 ** 7                                  # never reached: the clock stops it
+    p = SearchParams.defaults_for(qi[0].n_activities, total_iters=budget_iters, workers=workers,
+                                  seed=0)
+    cfg = SolveConfig(total_iters=budget_iters, workers=workers, pool_size=p.pool_size,
+                      tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
+                      phi_max=p.phi_max, seed=0, group=args.group, threads=args.threads,
+                      time_limit_s=0.97 * cb["wall"])
+    res = BatchSolver(qi, qm, cfg).run()
+    torch.cuda.synchronize()
     dev = float(np.mean(100.0 * (res.best_cmax - res.critical_path) / res.critical_path))
     return {"wall_budget_s": cb["wall"], "instances": K,
             "cpu": {"cpm_dev": cb["cpm_dev"], "iters_per_instance": cb["iters"],
                     "kind": "port", "workers_per_instance": cb.get("threads")},
-            "gpu": {"cpm_dev": dev, "iters_per_instance": budget,
-                    "workers_per_instance": workers, "device_s": res.device_ms * 1e-3}}
+            "gpu": {"cpm_dev": dev, "iters_per_instance": float(np.mean(res.iterations)),
+                    "workers_per_instance": workers, "device_s": res.device_ms * 1e-3,
+                    "stop": "device clock (%globaltimer), 97 % of the budget"}}
 
 
 def main() -> None:
@@ -464,7 +462,7 @@ def main() -> None:
                       f"I_total={cb['iters']}, {cores} worker threads each, "
                       f"{cb['wall']:.1f} s; cpm_dev {cb['cpm_dev']:.2f}%"}
         if not args.no_quality:
-            line["quality"] = quality_leg(args, insts, modes, cb, iters_done / (tot_ms * 1e-3))
+            line["quality"] = quality_leg(args, insts, modes, cb)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 4
+#define RCPSP_ABI_VERSION 5
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -86,8 +86,13 @@ typedef struct RcpspSolveArgs {
     int64_t cluster;            /* CTAs per worker (thread-block cluster,
                                  * 1..8): the leader CTA runs the search, the
                                  * others evaluate neighbourhood moves over
-                                 * distributed shared memory (TIME group 32
-                                 * only; others run with 1) */
+                                 * distributed shared memory (prefix-reusing
+                                 * evaluators; others run with 1) */
+    int64_t time_budget_ns;     /* > 0: wall-clock budget of the launch on the
+                                 * device clock (%globaltimer): no new grants
+                                 * and no further iterations once it is spent */
+    int64_t *t0_ns;             /* [1] launch start (atomicMin of every CTA's
+                                 * first clock read); host sets INT64_MAX */
 } RcpspSolveArgs;
 
 int rcpsp_abi_version(void);

@@ -15,7 +15,7 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _lib = None
 
@@ -46,7 +46,7 @@ class RcpspSolveArgs(ctypes.Structure):
         ("h_max", ctypes.c_int64), ("e_max", ctypes.c_int64), ("m_max", ctypes.c_int64),
         ("rmax_max", ctypes.c_int64), ("words", ctypes.c_int64), ("group", ctypes.c_int64),
         ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
-        ("cluster", ctypes.c_int64),
+        ("cluster", ctypes.c_int64), ("time_budget_ns", ctypes.c_int64), ("t0_ns", _vp),
     ]
 
 

@@ -536,6 +536,13 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
             A.moves_buf + static_cast<size_t>(wkr) * A.nbhd_max,
             A.cmax_buf + static_cast<size_t>(wkr) * A.nbhd_max, A.err);
   c.inc = A.full_sgs == 0;
+  if (A.time_budget_ns > 0) {
+    c.budget_ns = A.time_budget_ns;
+    c.t0_ns = reinterpret_cast<const long long*>(A.t0_ns);
+    if (tid == 0)
+      atomicMin(reinterpret_cast<unsigned long long*>(A.t0_ns),
+                static_cast<unsigned long long>(globaltimer()));
+  }
   if constexpr ((MODE == MODE_TIME && G == 32) || MODE == MODE_CAPACITY) {
     if (C > 1) {
       if (cluster_rank() != 0) {
@@ -604,6 +611,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
     if (tid == 0) {
       const long long best = ldcg64(&Hd[WS_BEST]);
       if (best <= ldcg64(&Hd[WS_FLOOR])) Hd[WS_STOP] = 1;
+      if (budget_spent(c.budget_ns, c.t0_ns)) Hd[WS_STOP] = 1;
       const long long planned = ldcg64(&Hd[WS_PLANNED]);
       if (ldcg64(&Hd[WS_STOP]) || planned >= A.epoch_limit) {
         c.scal[SC_NONE] = 1;

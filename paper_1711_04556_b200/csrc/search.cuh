@@ -45,6 +45,8 @@ struct CtaCtx {
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
   bool inc;        // TIME G = 32: reuse the current order's schedule prefix
   int csize;       // CTAs of this worker's cluster (1: no cluster); this CTA is the leader
+  long long budget_ns;         // > 0: wall-clock budget of the launch (device clock)
+  const long long* t0_ns;      // launch start
   uint32_t* moves_buf;  // global [nbhd] compacted moves
   int* cmax_buf;        // global [nbhd] makespans
   int* err;
@@ -306,6 +308,13 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
 }
+// the launch's wall-clock budget is spent (device clock, %globaltimer)
+__device__ __forceinline__ bool budget_spent(long long budget_ns, const long long* t0_ns) {
+  if (budget_ns <= 0) return false;
+  const long long t0 = *reinterpret_cast<const volatile long long*>(t0_ns);
+  return static_cast<long long>(globaltimer()) - t0 >= budget_ns;
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -944,6 +953,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
       c.scal[SC_HEAD] = tabu_add1(c, c.scal[SC_HEAD], u, v);
       if (trace) trace[iters - 1] = cur;
       c.scal[SC_BSTOK] = (c.cmax_buf[pick] & CONV_FLAG) ? 1 : 0;
+      c.scal[SC_FLAG] = budget_spent(c.budget_ns, c.t0_ns) ? 1 : 0;
     }
     __syncthreads();
     if (cur < local_best) {
@@ -952,6 +962,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     }
     if (local_best < adopted_cmax) break;
     if (local_best <= floor_cmax) break;
+    if (c.scal[SC_FLAG]) break;  // wall-clock budget spent (only with a budget)
   }
   __syncthreads();
   ChunkOut o;
@@ -1062,6 +1073,8 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.bst = smem + p.bst;
   c.inc = true;
   c.csize = 1;
+  c.budget_ns = 0;
+  c.t0_ns = nullptr;
   c.tabu_list = reinterpret_cast<uint32_t*>(smem + p.tabu_list);
   c.tabu_cnt = reinterpret_cast<uint32_t*>(smem + p.tabu_cnt);
   c.red = smem + p.red;

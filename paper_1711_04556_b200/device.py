@@ -428,6 +428,7 @@ class SolveConfig:
     full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluators
     cap_group: int | None = None  # CAPACITY: 32 = warp, 1 = thread per schedule, None = auto
     cluster: int | None = None    # CTAs per worker (1..8; TIME group 32), None = auto
+    time_limit_s: float | None = None  # wall-clock budget of the search on the device clock
 
     @property
     def block_iters(self) -> int:
@@ -518,6 +519,7 @@ class BatchSolver:
         self.moves_buf = z((grid_max, self.nbhd_max), i32)
         self.cmax_buf = z((grid_max, self.nbhd_max), i32)
         self.err = z(1, i32)
+        self.t0 = torch.full((1,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda")
         self.d_pool_rng = z((I, 6), i64)
         self.d_ids = {k: z(len(v), i32) for k, v in groups.items()}
         self.launches = 0
@@ -546,6 +548,7 @@ class BatchSolver:
                   self.err):
             t.zero_()
         self.w_rng.copy_(_torch().from_numpy(self.w_rng_host.view(np.int64)).cuda())
+        self.t0.fill_(np.iinfo(np.int64).max)
         if self.w_trace is not None:
             self.w_trace.zero_()
             self.w_chunks.zero_()
@@ -584,6 +587,8 @@ class BatchSolver:
             self.instances)
         a.cluster = (cfg.cluster if cfg.cluster is not None
                      else pick_cluster(n_group * cfg.workers))
+        a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
+        a.t0_ns = ptr(self.t0)
         return a
 
     def pool_init(self, stream=None) -> None:

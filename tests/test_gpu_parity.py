@@ -454,3 +454,22 @@ def test_cluster_workers_equal_single_cta():
                       phi_steps=20, phi_max=3, seed=2, cluster=4)
     r = BatchSolver(insts, [1] * 4, cfg).run()
     assert r.iterations.tolist() == [300] * 4
+
+
+def test_time_limited_solve_stops_on_the_device_clock():
+    """SolveConfig.time_limit_s: the search stops on %globaltimer -- well before
+    the iteration budget, close to the time limit -- and the result is a valid
+    schedule (the budget's only effect is where the search stops)."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts = synth.benchmark_batch("j120p", 6, first_seed=20)
+    cfg = SolveConfig(total_iters=10 ** 7, workers=4, pool_size=8, tabu_size=800, delta=60,
+                      phi_steps=20, phi_max=3, seed=1, time_limit_s=0.4)
+    r = BatchSolver(insts, [1] * 6, cfg).run()
+    assert 0.3 < r.search_ms * 1e-3 < 1.0
+    assert (r.iterations < 10 ** 7).all()
+    # an instance the pool already solved to the critical path never searches
+    assert ((r.iterations > 0) | (r.best_cmax == r.critical_path)).all()
+    for i, inst in enumerate(insts):
+        from paper_1711_04556_b200 import evaluate
+        n = inst.n_activities
+        assert evaluate(r.best_order[i, :n], inst, 1).cmax == int(r.best_cmax[i])
