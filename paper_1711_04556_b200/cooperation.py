@@ -248,19 +248,25 @@ def _finish(instance: ProjectInstance, res: device.BatchResult, i: int, params: 
 
 
 def orchestrate(instance: ProjectInstance, params: SearchParams, mode: EvalMode | None = None,
-                mode_controller: DynamicModeController | None = None) -> RunStats:
+                mode_controller: DynamicModeController | None = None,
+                time_limit_s: float | None = None) -> RunStats:
     """Solve one instance on the GPU with `params.workers` CTAs (cooperation.py:431-496).
 
     With B = 1 and a pinned mode the trajectory (trace, evaluations,
     exchanges, best) is identical to the reference.  A dynamic controller
     (B = 1, 'auto-measure') re-measures the modes on the GPU between search
     epochs of `measure_window` granted iterations, the grant cap the
-    reference applies in that mode."""
+    reference applies in that mode.
+
+    time_limit_s (an extension; the reference has no time stop): the search
+    also stops when this much device time has passed (%globaltimer), like a
+    solver's wall-clock limit."""
     if mode is None:
         mode = params.mode
     if mode_controller is not None and params.workers == 1:
         return _orchestrate_dynamic(instance, params, mode_controller)
-    solver = device.BatchSolver([instance], [int(mode)], _solve_config(params))
+    solver = device.BatchSolver([instance], [int(mode)],
+                                _solve_config(params, time_limit_s=time_limit_s))
     res = solver.run()
     return _finish(instance, res, 0, params, EvalMode(mode).name, res.device_ms * 1e-3)
 
@@ -322,7 +328,8 @@ class BatchStats:
 
 def orchestrate_batch(instances: list[ProjectInstance], params: SearchParams,
                       modes: list[EvalMode] | None = None, rules=DEFAULT_RULES,
-                      group: int | None = None, threads: int = 0) -> BatchStats:
+                      group: int | None = None, threads: int = 0,
+                      time_limit_s: float | None = None) -> BatchStats:
     """Solve many instances at once: each gets its own working set and
     `params.workers` CTAs; all run concurrently on the GPU.  Modes default
     to the static rules per instance (BASELINE config: heuristic selection)."""
@@ -330,7 +337,8 @@ def orchestrate_batch(instances: list[ProjectInstance], params: SearchParams,
         modes = [decide_static(extract_features(x), rules) for x in instances]
     tick = time.perf_counter()
     solver = device.BatchSolver(instances, [int(m) for m in modes],
-                                _solve_config(params, group=group, threads=threads))
+                                _solve_config(params, group=group, threads=threads,
+                                              time_limit_s=time_limit_s))
     res = solver.run()
     wall = time.perf_counter() - tick
     dev_s = res.device_ms * 1e-3
