@@ -296,8 +296,7 @@ def _orchestrate_dynamic(instance: ProjectInstance, params: SearchParams,
         new_mode = ctl.mode_for(int(hdr[device.WS_FIELDS["consumed"]]))
         if new_mode != mode:
             mode = new_mode
-            solver.groups = {(int(mode), k[1] if int(mode) == 1 else 1): v
-                             for k, v in solver.groups.items()}
+            solver.groups = {(int(mode), k[1]): v for k, v in solver.groups.items()}
             solver.d_ids = {k: solver.d_ids[old] for k, old in
                             zip(solver.groups, list(solver.d_ids))}
         ev0.record()

@@ -488,7 +488,8 @@ class BatchSolver:
             raise UnsupportedInstance(f"neighbourhood of {self.nbhd_max} moves >= {KEY_LIMIT}")
         groups: dict[tuple[int, int], list[int]] = {}
         for i, b in enumerate(blobs):
-            key = (self.modes[i], int(b[B_W]) if self.modes[i] == MODE_TIME else 1)
+            # the packing words size every kernel's instance staging, in both modes
+            key = (self.modes[i], int(b[B_W]))
             groups.setdefault(key, []).append(i)
         self.groups = groups
         seeds = pool_seeds if pool_seeds is not None else [cfg.seed] * I

@@ -440,6 +440,9 @@ def test_cluster_workers_equal_single_cta():
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     insts = synth.benchmark_batch("j120p", 3, first_seed=150) + \
         synth.benchmark_batch("j60", 1, first_seed=3)
+    # two-word packing (6 resources) with durations > 32 (the multi-round paths)
+    wide = synth.random_instance(50, 6, seed=91, cap_lo=20, cap_hi=60, max_dur=45,
+                                 demand_density=0.6)
     for modes, cap_group in (([1] * 4, None), ([1, 0, 0, 1], 32), ([0, 1, 0, 0], 1)):
         out = []
         for cl in (1, 2, 8):
@@ -450,6 +453,19 @@ def test_cluster_workers_equal_single_cta():
             out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
                         [[t.tolist() for t in tr] for tr in r.traces]))
         assert out[0] == out[1] == out[2], (modes, cap_group)
+    for mode in (1, 0):
+        out = []
+        for cl in (1, 4):
+            cfg = SolveConfig(total_iters=60, workers=1, pool_size=8, tabu_size=250, delta=60,
+                              phi_steps=20, phi_max=3, seed=5, collect_trace=True, cluster=cl)
+            r = BatchSolver([wide], [mode], cfg).run()
+            out.append((r.best_cmax.tolist(), r.evaluations.tolist(),
+                        [[t.tolist() for t in tr] for tr in r.traces]))
+        assert out[0] == out[1], ("wide", mode)
+        want = oracle.orchestrate(wide, 60, 1, 5, mode, delta=60, tabu_size=250,
+                                  pool_size=8, collect_trace=True)
+        assert out[0][0] == [want["best_cmax"]] and out[0][1] == [want["evaluations"]]
+        assert out[0][2][0] == [t.tolist() for t in want["traces"]], ("wide", mode)
     cfg = SolveConfig(total_iters=300, workers=3, pool_size=8, tabu_size=800, delta=60,
                       phi_steps=20, phi_max=3, seed=2, cluster=4)
     r = BatchSolver(insts, [1] * 4, cfg).run()
