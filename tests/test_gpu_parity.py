@@ -489,3 +489,31 @@ def test_time_limited_solve_stops_on_the_device_clock():
         from paper_1711_04556_b200 import evaluate
         n = inst.n_activities
         assert evaluate(r.best_order[i, :n], inst, 1).cmax == int(r.best_cmax[i])
+
+
+def test_batch_solve_shapes_vs_oracle():
+    """Full B = 1 solves of varied shapes (1-8 resources, 8/16-bit packings,
+    long durations, sparse demand) in one mixed batch: traces, evaluations and
+    best makespans equal the oracle's for every instance and mode."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    rng = np.random.default_rng(43)
+    insts, modes = [], []
+    for seed in range(12):
+        m = int(rng.integers(1, 9))
+        cap_hi = int(rng.choice([6, 20, 127, 300]))
+        if m > 4 and cap_hi > 127:
+            cap_hi = 127
+        insts.append(synth.random_instance(int(rng.integers(8, 60)), m, seed=300 + seed,
+                                           cap_lo=max(1, cap_hi // 3), cap_hi=cap_hi,
+                                           max_dur=int(rng.choice([5, 10, 40])),
+                                           demand_density=float(rng.choice([0.3, 0.7]))))
+        modes.append(seed % 2)
+    cfg = SolveConfig(total_iters=40, workers=1, pool_size=6, tabu_size=60, delta=30,
+                      phi_steps=20, phi_max=3, seed=7, collect_trace=True)
+    r = BatchSolver(insts, modes, cfg).run()
+    for i, (inst, mode) in enumerate(zip(insts, modes)):
+        want = oracle.orchestrate(inst, 40, 1, 7, mode, delta=30, tabu_size=60, pool_size=6,
+                                  collect_trace=True)
+        assert int(r.best_cmax[i]) == want["best_cmax"], (i, mode)
+        assert int(r.evaluations[i]) == want["evaluations"], (i, mode)
+        assert [t.tolist() for t in r.traces[i]] == [t.tolist() for t in want["traces"]], i
