@@ -517,3 +517,33 @@ def test_batch_solve_shapes_vs_oracle():
         assert int(r.best_cmax[i]) == want["best_cmax"], (i, mode)
         assert int(r.evaluations[i]) == want["evaluations"], (i, mode)
         assert [t.tolist() for t in r.traces[i]] == [t.tolist() for t in want["traces"]], i
+
+
+def test_multi_worker_batch_shapes_feasible():
+    """B > 1 with steals (and clusters where the launch is small) over varied
+    shapes: every instance consumes exactly its budget (or stops at the
+    critical path) and its best order's schedule is feasible with the
+    reported makespan."""
+    from paper_1711_04556_b200 import evaluate
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    rng = np.random.default_rng(47)
+    insts, modes = [], []
+    for seed in range(10):
+        m = int(rng.integers(1, 7))
+        cap_hi = int(rng.choice([8, 30, 120]))
+        insts.append(synth.random_instance(int(rng.integers(10, 70)), m, seed=400 + seed,
+                                           cap_lo=max(1, cap_hi // 3), cap_hi=cap_hi,
+                                           max_dur=int(rng.choice([8, 36])),
+                                           demand_density=0.6))
+        modes.append(int(rng.integers(0, 2)))
+    for cluster in (None, 1):
+        cfg = SolveConfig(total_iters=150, workers=3, pool_size=6, tabu_size=60, delta=30,
+                          phi_steps=20, phi_max=3, seed=11, cluster=cluster)
+        r = BatchSolver(insts, modes, cfg).run()
+        for i, (inst, mode) in enumerate(zip(insts, modes)):
+            assert r.iterations[i] == 150 or r.best_cmax[i] == r.critical_path[i], i
+            n = inst.n_activities
+            sched = evaluate(r.best_order[i, :n], inst, mode)
+            assert sched.cmax == int(r.best_cmax[i]), (i, mode)
+            ok, problems = check_schedule_feasible(inst, sched)
+            assert ok, (i, problems[:3])
