@@ -547,3 +547,40 @@ def test_multi_worker_batch_shapes_feasible():
             assert sched.cmax == int(r.best_cmax[i]), (i, mode)
             ok, problems = check_schedule_feasible(inst, sched)
             assert ok, (i, problems[:3])
+
+
+def test_reference_backend_fingerprint(golden):
+    """The reference's own backend-parity harness (helpers.py:190-223,
+    test_backends.py:36-41) with this package as the backend: the same digest
+    -- evaluations in both modes, filters, forward-backward improvement and a
+    200-iteration seeded search trace -- recomputed through this package's
+    API on the GPU equals the one the reference produced with numba
+    (tests/golden/fingerprint.json, tests/golden/make_fingerprint.py)."""
+    import json
+    from conftest import ROOT
+    from paper_1711_04556_b200 import (filter_infeasible, forward_backward_improve,
+                                       generate_reduced_neighborhood)
+    want = json.loads((ROOT / "tests" / "golden" / "fingerprint.json").read_text())
+    out: dict = {}
+    rng = np.random.default_rng(2024)
+    evals, filters = [], []
+    for seed in range(6):
+        inst = synth.random_instance(12, 2, seed=seed)
+        order = random_topological_order(inst, rng)
+        for mode in (0, 1):
+            sched = evaluate(order, inst, mode)
+            evals.append([sched.cmax] + sched.starts.tolist())
+        moves = generate_reduced_neighborhood(order, 8)
+        filters.append(filter_infeasible(moves, order, inst).tolist())
+        improved, sched = forward_backward_improve(inst, order, 1)
+        evals.append([sched.cmax] + improved.tolist())
+    out["evals"] = evals
+    out["filters"] = filters
+    inst = synth.random_instance(14, 3, seed=99)
+    params = SearchParams.defaults_for(16, total_iters=200, workers=1, seed=5,
+                                       collect_trace=True)
+    stats = orchestrate(inst, params)
+    out["search_best"] = stats.best_cmax
+    out["search_evals"] = stats.evaluations
+    out["search_trace"] = [int(x) for chunk in stats.traces for x in chunk]
+    assert json.loads(json.dumps(out)) == want
