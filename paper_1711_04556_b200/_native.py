@@ -11,10 +11,14 @@ g; g.build()"` (or `make -C paper_1711_04556_b200`).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
+# A/B measurements of kernel variants (tools/ab_bench.sh) point this at another build
+if os.environ.get("RCPSP_B200_LIB"):
+    LIB_PATH = Path(os.environ["RCPSP_B200_LIB"])
 ABI_VERSION = 5
 
 _lib = None

@@ -62,7 +62,7 @@ struct SInst {
 };
 
 __host__ __device__ __forceinline__ int inst_smem_words(int n, int m, int e, int W) {
-  return 8 * n + n + n * W + n * m + m + W + 2 * (n + 1) + 2 * e;
+  return 8 * n + n + n * W + n * m + m + W + 2 * (n + 1) + 2 * e + 32;  // + pdat padding
 }
 
 // y &= y >> s_i (i = 1..5) turns a slot mask into "a run of d ones starts
@@ -127,6 +127,10 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
   I.capw = reinterpret_cast<const uint32_t*>(copy(blob[B_OFF_CAPW], W));
   I.pptr = copy(blob[B_OFF_PPTR], n + 1);
   I.pdat = copy(blob[B_OFF_PDAT], e);
+  // 32 zero entries after the predecessor lists: a warp may read a whole
+  // 32-lane window from any span start (lanes past the span read activity 0)
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) p[i] = 0;
+  p += 32;
   I.sptr = copy(blob[B_OFF_SPTR], n + 1);
   I.sdat = copy(blob[B_OFF_SDAT], e);
   return static_cast<int>(p - smem);

@@ -234,8 +234,10 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
                                               int& hw, int& cmax, int* err) {
   const int lane = threadIdx.x & 31;
   const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
-  const bool pl = lane < pc;
-  int f = static_cast<int>(lds32_if(pl, a_fin + 4 * lds32_if(pl, a_pdat + 4 * (p0 + lane), 0u), 0u));
+  // the predecessor lists are padded by 32 entries (common.cuh): every lane
+  // loads, lanes past the span are masked
+  int f = static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + lane))));
+  f = lane < pc ? f : 0;
   if (BIG && pc > 32)
     for (int e = lane + 32; e < pc; e += 32)
       f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
