@@ -111,7 +111,10 @@ __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, in
   return __ballot_sync(FULL_MASK, t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi)));
 }
 
-template <int W>
+// BIG = false (every duration <= 32): a lane whose window would end past the
+// round cannot hit -- m >> lane brings in zeros, and dmask covers them -- so
+// the candidate test is implied.
+template <int W, bool BIG = true>
 __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
                                            uint32_t hi, int esv, int dur, uint32_t dmask,
@@ -119,7 +122,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   const int lane = threadIdx.x & 31;
   // lane i tests the window [t0+i, t0+i+dur) inside the round: a candidate
   // iff it ends in the round, a hit iff dur fitting slots start at bit i
-  const bool cand = lane + dur <= 32;
+  const bool cand = !BIG || lane + dur <= 32;
   // first round, peeled: nothing is carried in, so lane 0's test covers the
   // window starting at esv
   uint32_t m = window_fits_ballot<W>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
@@ -149,11 +152,16 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
                                             uint32_t cap1) {
   const int lane = threadIdx.x & 31;
   const int fin = start + dur;
-  if (start > hw)
-    for (int t = hw + lane; t < start; t += 32) {
+  const int gap = start - hw;
+  if (gap > 0) {  // materialise [hw, start): one predicated store per lane, a loop past 32
+    const uint32_t adr = a_tau + 4 * W * (hw + lane);
+    sts32_if(lane < gap, adr, cap0);
+    if (W == 2) sts32_if(lane < gap, adr + 4, cap1);
+    for (int t = hw + 32 + lane; t < start; t += 32) {
       sts32(a_tau + 4 * W * t, cap0);
       if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
     }
+  }
   const int t = start + lane;  // one slot per lane (a loop only for dur > 32)
   {
     const uint32_t adr = a_tau + 4 * W * t;
@@ -204,8 +212,8 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
   int start = esv;
   if (dur > 0 && (r0 | r1) != 0) {
     if (esv < hw)
-      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
-                                static_cast<uint32_t>(rec.w), err);
+      start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                     static_cast<uint32_t>(rec.w), err);
     warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
@@ -248,8 +256,8 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   int start = esv;
   if (dur > 0 && (r0 | r1) != 0) {
     if (esv < hw)
-      start = warp_window<W>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
-                             static_cast<uint32_t>(rec.w), err);
+      start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                  static_cast<uint32_t>(rec.w), err);
     warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
