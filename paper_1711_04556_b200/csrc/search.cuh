@@ -344,7 +344,8 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | fin [n] | log [2n] | ord [n]
+//   per-warp scratch: tau (H+1)*W | fin [n] | log [2n] | ord [n + 1] (ord[n]: a
+//   valid pad the unrolled loop's prefetch may read)
 // The log lists the suffix bookings below hw_pre -- (start | dur << 16,
 // packed demand (W = 1) or activity (W = 2)) -- the only ones the undo has to
 // give back (a zero demand gives back nothing).
@@ -366,6 +367,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
                  a_tau = sa(ws), a_fin = sa(ws + (H + 1) * W),
                  a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + 8 * n;
+  if (lane == 0) sts32(a_ord + 4 * n, 0u);
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
   // the last position holds the sink (every activity precedes it, and moves
   // never reach it): with zero duration it starts at max(es) <= cm, so it
@@ -437,13 +439,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       int act_a = act;
       int4 rec_a = rec;
       for (;;) {
-        const int act_b = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // ord[n]: pad
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
                                           a_tau, a_fin, hw, cm, err);
         log_below(act_a, rec_a, st);
         if (++p >= pend) break;
-        act_a = static_cast<int>(lds32(a_ord + 4 * min(p + 1, n - 1)));
+        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_pull<W, BIG>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
                                       a_fin, hw, cm, err);
@@ -1026,7 +1028,7 @@ struct SmemPlan {
 
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n + 2 : (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1) * W + 4 * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return cap_lanes * cap_thread_words(n, m, rmax) + cap_warp_words(n, m, rmax);
 }
