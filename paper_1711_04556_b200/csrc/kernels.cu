@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, i
   if (op == OP_TIME_ES) {
     int start = arg;  // dur == 0 or es_prec >= H: the reference returns es_prec
     if (dur > 0 && arg < H)
-      start = warp_window<W>(sa(tau), H + 1, H, r0, r1, cap0, cap1, I.hi, arg, dur,
+      start = warp_window<W, true, true>(sa(tau), H + 1, H, r0, r1, cap0, cap1, I.hi, arg, dur,
                              window_mask(dur), nullptr);
     if (lane == 0) out[0] = start;
     return;

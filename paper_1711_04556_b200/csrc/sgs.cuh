@@ -99,7 +99,7 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 // first t >= esv with [t, t+dur) fitting, slots >= hw at capacity, t+dur <= H.
 // Each round tests 32 slots and resolves the window branch-free: the run
 // carried from the previous round, else the first run of `dur` ones.
-template <int W>
+template <int W, bool HCHK>
 __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
                                                        uint32_t r0, uint32_t r1, uint32_t cap0,
                                                        uint32_t cap1, uint32_t hi) {
@@ -108,13 +108,19 @@ __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, in
     w0 = lds32(a_tau + 4 * W * t);
     if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
   }
-  return __ballot_sync(FULL_MASK, t < H && fits1(w0, r0, hi) && (W == 1 || fits1(w1, r1, hi)));
+  // HCHK = false (the SGS): no t < H test -- packing rejects demands above
+  // capacity, so every activity fits from hw on (slots >= hw are free) and no
+  // window reaches past hw + dur <= H; the scan loop keeps its t0 >= H guard.
+  // The single-step state operation (arbitrary states) keeps the test, as the
+  // reference's scan stops at the horizon (kernels.py:127).
+  return __ballot_sync(FULL_MASK, (!HCHK || t < H) && fits1(w0, r0, hi) &&
+                                      (W == 1 || fits1(w1, r1, hi)));
 }
 
 // BIG = false (every duration <= 32): a lane whose window would end past the
 // round cannot hit -- m >> lane brings in zeros, and dmask covers them -- so
 // the candidate test is implied.
-template <int W, bool BIG = true>
+template <int W, bool BIG = true, bool HCHK = false>
 __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
                                            uint32_t hi, int esv, int dur, uint32_t dmask,
@@ -125,7 +131,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   const bool cand = !BIG || lane + dur <= 32;
   // first round, peeled: nothing is carried in, so lane 0's test covers the
   // window starting at esv
-  uint32_t m = window_fits_ballot<W>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
+  uint32_t m = window_fits_ballot<W, HCHK>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
   uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
   if (y) return esv + __ffs(y) - 1;
   int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
@@ -135,7 +141,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
       if (lane == 0) set_err(err, DE_NO_WINDOW);
       return H;
     }
-    m = window_fits_ballot<W>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
+    m = window_fits_ballot<W, HCHK>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
     const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
     if (carry + tz >= dur) return t0 - carry;
     y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
