@@ -233,3 +233,23 @@ def test_b200_rules_match_measurements():
     f = SimpleNamespace(max_capacity=16, avg_duration=5.5, min_capacity=10, avg_capacity=13,
                         avg_branch_factor=1.5, critical_path_length=0)
     assert decide_static(f, B200_RULES) == decide_static(f, DEFAULT_RULES) == EvalMode.TIME
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference algorithm on the host cores)
+    prints one JSON line with the driver's keys; it needs no GPU."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--config", "j30p", "--instances", "40", "--steps", "1",
+                          "--warmup", "0", "--cpu-seconds", "1", "--iters", "50"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
