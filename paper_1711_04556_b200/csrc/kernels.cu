@@ -129,12 +129,22 @@ __global__ void __launch_bounds__(512, 2) k_run_chunk(
     const int* __restrict__ blob, int delta, int T, int* orders, uint32_t* tabu, int* heads,
     const int* budget, const int* adopted, const int* start_cmax, const int* best_known,
     int floor_cmax, int* best_orders, int* trace, int trace_cap, long long* stats,
-    uint32_t* moves_buf, int* cmax_buf, int nbhd_max, SmemPlan plan, int* err) {
+    uint32_t* moves_buf, int* cmax_buf, int nbhd_max, SmemPlan plan, int* err, int C) {
   int* smem = dsm;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x / C;  // search index; C > 1: a cluster of CTAs per search
   CtaCtx c;
   cta_setup(c, blob, smem, plan, delta, T, moves_buf + static_cast<size_t>(b) * nbhd_max,
             cmax_buf + static_cast<size_t>(b) * nbhd_max, err);
+  if constexpr ((MODE == MODE_TIME && G == 32) || MODE == MODE_CAPACITY) {
+    if (C > 1) {
+      if (cluster_rank() != 0) {
+        cta_follow<MODE, G, W>(c, blob, nullptr, 0, smem, plan.inst, C);
+        return;
+      }
+      c.csize = C;
+      if (threadIdx.x == 0) c.scal[SC_IID] = 0;
+    }
+  }
   const int n = c.I.n;
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
     c.base[p] = orders[static_cast<size_t>(b) * n + p];
@@ -147,6 +157,12 @@ __global__ void __launch_bounds__(512, 2) k_run_chunk(
   ChunkOut o = run_chunk_cta<MODE, G, W>(c, budget[b], adopted[b], start_cmax[b], best_known[b],
                                          floor_cmax,
                                          trace ? trace + static_cast<size_t>(b) * trace_cap : nullptr);
+  if (c.csize > 1) {  // release the followers; keep this CTA alive until they are out
+    if (threadIdx.x == 0) c.scal[SC_CMD] = CMD_DONE;
+    __syncthreads();
+    cluster_sync_all();
+    cluster_sync_all();
+  }
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
     orders[static_cast<size_t>(b) * n + p] = c.base[p];
     best_orders[static_cast<size_t>(b) * n + p] = c.best[p];
@@ -546,7 +562,7 @@ __global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* _
   if constexpr ((MODE == MODE_TIME && G == 32) || MODE == MODE_CAPACITY) {
     if (C > 1) {
       if (cluster_rank() != 0) {
-        cta_follow<MODE, G, W>(c, A, iid, smem, plan.inst, C);
+        cta_follow<MODE, G, W>(c, A.blob, A.blob_off, iid, smem, plan.inst, C);
         return;
       }
       c.csize = C;
@@ -995,10 +1011,36 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
       return fail("search state does not fit in shared memory");
     auto k = k_run_chunk<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
-    k<<<batch, nt, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
-                                          adopted, start_cmax, best_known, floor_cmax, best_orders,
-                                          trace, trace_cap, reinterpret_cast<long long*>(stats),
-                                          moves_buf, cmax_buf, nbhd_max, p, err);
+    // a small batch leaves SMs idle: spread each search over a cluster of up
+    // to 8 CTAs when its evaluator deals moves from a shared counter
+    const bool shared_counter = MODE == MODE_TIME ? G == 32 : (G == 32 || h.n >= 48);
+    int C = shared_counter ? std::min(8, std::max(1, 2 * sm_count() / batch)) : 1;
+    if (C == 1) {
+      k<<<batch, nt, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
+                                            adopted, start_cmax, best_known, floor_cmax,
+                                            best_orders, trace, trace_cap,
+                                            reinterpret_cast<long long*>(stats), moves_buf,
+                                            cmax_buf, nbhd_max, p, err, 1);
+      return launch_check("k_run_chunk");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * C);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = p.total * 4;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cuda_check(cudaLaunchKernelEx(&cfg, k, blob, delta, tabu_size, orders, tabu, heads, budget,
+                                      adopted, start_cmax, best_known, floor_cmax, best_orders,
+                                      trace, trace_cap, reinterpret_cast<long long*>(stats),
+                                      moves_buf, cmax_buf, nbhd_max, p, err, C),
+                   "k_run_chunk (cluster)"))
+      return -1;
     return launch_check("k_run_chunk");
   });
 }

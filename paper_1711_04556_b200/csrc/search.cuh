@@ -744,8 +744,9 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
 // memory, deal moves from the leader's counter, write makespans into the
 // leader's global buffer, B2.  The instance follows the leader's (steals).
 template <int MODE, int G, int W>
-__device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* smem, int plan_inst,
-                           int csize) {
+//   blob/blob_off: the launch's instances (blob_off null: one instance)
+__device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, int iid, int* smem,
+                           int plan_inst, int csize) {
   const int tid = threadIdx.x;
   const uint32_t l_scal = cluster_map(sa(c.scal), 0);
   const uint32_t l_base = cluster_map(sa(c.base), 0), l_bst = cluster_map(sa(c.bst), 0);
@@ -754,9 +755,9 @@ __device__ void cta_follow(CtaCtx& c, const RcpspSolveArgs& A, int iid, int* sme
     const int cmd = static_cast<int>(ld_cluster(l_scal + 4 * SC_CMD));
     if (cmd == CMD_DONE) break;
     const int liid = static_cast<int>(ld_cluster(l_scal + 4 * SC_IID));
-    if (liid != iid) {
+    if (blob_off != nullptr && liid != iid) {
       iid = liid;
-      stage_instance(A.blob + A.blob_off[iid], smem + plan_inst, c.I);
+      stage_instance(blob + blob_off[iid], smem + plan_inst, c.I);
     }
     const int n_feas = static_cast<int>(ld_cluster(l_scal + 4 * SC_NF));
     const int base_cmax = static_cast<int>(ld_cluster(l_scal + 4 * SC_BASEC));
