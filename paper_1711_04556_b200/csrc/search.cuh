@@ -518,7 +518,7 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req,
 // of starts), so there is no undo and no convergence exit: each move copies
 // the prefix state (c_pre, es_pre) and schedules positions u..n-1.  With
 // reuse == false the prefix stays empty (full SGS of every swapped order).
-//   per-warp scratch: c [m*rs] | cb [rs] | es [n] | c_pre [m*rs] | es_pre [n]
+//   per-warp scratch: c [m*rs] | cb [m*rs] | es [n] | c_pre [m*rs] | es_pre [n]
 __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_dem, int o_cap,
                                                  int o_base, int o_bst, int o_ctr, int o_evs,
                                                  int n, int m, int rs,
@@ -528,7 +528,7 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mr = m * rs;
   const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
-  const uint32_t a_c = a_scr, a_cb = a_c + 4 * mr, a_es = a_cb + 4 * rs, a_cp = a_es + 4 * n,
+  const uint32_t a_c = a_scr, a_cb = a_c + 4 * mr, a_es = a_cb + 4 * mr, a_cp = a_es + 4 * n,
                  a_esp = a_cp + 4 * mr;
   const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr);
@@ -615,7 +615,7 @@ __device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_ev
 // swapped order; positions u_min..u-1 are the current order's, booked at their
 // known starts.
 //   per-warp scratch: L lanes x (c [m*R] | cb [R] | es [n]) interleaved by lane
-//                     | c_pre [m*rs] | cb_w [rs] | es_pre [n]
+//                     | c_pre [m*rs] | cb_w [m*rs] | es_pre [n]
 __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_base, int o_bst,
                                                        int o_ctr, int o_evs,
                                                        const uint32_t* __restrict__ moves,
@@ -628,7 +628,7 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
   const int* bst = dsm + o_bst;
   int* st = dsm + o_evs + warp * warp_words;
   int* cpre = st + L * cap_thread_words(n, m, R);
-  int* esp = cpre + (m + 1) * rs;
+  int* esp = cpre + 2 * m * rs;
   const uint32_t a_cpre = sa(cpre), a_cbw = sa(cpre + m * rs), a_dem = sa(I.dem),
                  a_ctr = sa(dsm + o_ctr);
   const int capk = lane < m ? I.cap[lane] : 0;

@@ -503,12 +503,12 @@ __host__ __device__ __forceinline__ int cap_thread_words(int n, int m, int rmax)
 // buffer -- so Eq. 7's max over resources is one REDUX and the m Alg. 4
 // updates run side by side.  Rows are `rs` words apart (rmax rounded up to
 // odd: the m rows fall in distinct banks).
-//   scratch: c [m*rs] | cb [rs] | es [n]
+//   scratch: c [m*rs] | cb [m*rs] | es [n]
 
 __host__ __device__ __forceinline__ int cap_row_stride(int rmax) { return rmax | 1; }
 
 __host__ __device__ __forceinline__ int cap_warp_words(int n, int m, int rmax) {
-  return (m + 1) * cap_row_stride(rmax) + n;
+  return 2 * m * cap_row_stride(rmax) + n;  // c rows | copy-buffer rows | es
 }
 
 // Alg. 4 (kernels.py:81-110) on one resource row from entry i0 on, one
@@ -573,8 +573,61 @@ __device__ __forceinline__ void cap_commit_warp(uint32_t a_c, uint32_t a_cb, int
 
 // The m resource updates of one activity, one after another, whole warp.
 // req: lane k < m holds resource k's demand.
+// Alg. 4 for up to 4 resources at once: lanes 8k..8k+7 own resource k (its
+// state row and copy-buffer row).  The leading run of entries >= start + dur
+// is found by strided probing (8 probes per round narrow the range 8x; the
+// row is descending, so the probe verdicts are monotone), then the same fast
+// path / reference loop as cap_commit_warp.
+__device__ __forceinline__ void cap_commit_groups(uint32_t a_c, uint32_t a_cb, int rs, int m,
+                                                  int capk_k, int req_k, int start, int dur) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  const int capk = __shfl_sync(FULL_MASK, capk_k, g);
+  const int req = __shfl_sync(FULL_MASK, req_k, g);
+  const bool act = g < m && req > 0;
+  const uint32_t row = a_c + 4 * g * rs, cbrow = a_cb + 4 * g * rs;
+  const int T = start + dur;
+  int lo = 0, hi = act ? capk : 0;  // first entry < T lies in [lo, hi), or there is none
+  while (__any_sync(FULL_MASK, hi - lo > 8)) {
+    const int span = hi - lo;
+    const bool nar = span > 8;
+    const int stride = (span + 7) >> 3;
+    const int idx = lo + j * stride;
+    const bool pr = nar && idx < hi && static_cast<int>(lds32(row + 4 * idx)) < T;
+    const uint32_t b = (__ballot_sync(FULL_MASK, pr) >> (8 * g)) & 0xffu;
+    if (nar) {
+      if (b) {
+        const int f = __ffs(b) - 1;  // first probe below T: the entry lies in (probe f-1, probe f]
+        hi = lo + f * stride + 1;
+        lo = f > 0 ? lo + (f - 1) * stride + 1 : lo;
+      } else {  // every probe inside the range is at or above T: past the last one
+        lo += min(7, (span - 1) / stride) * stride + 1;
+      }
+    }
+  }
+  const bool pr = j < hi - lo && static_cast<int>(lds32(row + 4 * (lo + j))) < T;
+  const uint32_t b = (__ballot_sync(FULL_MASK, pr) >> (8 * g)) & 0xffu;
+  const int i0 = b ? lo + __ffs(b) - 1 : capk;
+  if (act && i0 < capk) {
+    const int c0 = static_cast<int>(lds32(row + 4 * i0));
+    if (c0 <= start && i0 + req <= capk) {
+      for (int t = j; t < req; t += 8) sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
+    } else if (j == 0) {
+      cap_commit_row(row, cbrow, capk, req, start, dur, i0);
+    }
+  }
+  __syncwarp();
+}
+
+// The m resource updates of one activity: side by side for m <= 4
+// (cap_commit_groups), else one after another with the whole warp.
+//   a_cb: m copy-buffer rows, rs words apart
 __device__ __forceinline__ void cap_commit_all(uint32_t a_c, uint32_t a_cb, int rs, int m,
                                                int capk, int req, int start, int dur) {
+  if (m <= 4) {
+    cap_commit_groups(a_c, a_cb, rs, m, capk, req, start, dur);
+    return;
+  }
   for (int k = 0; k < m; ++k) {
     const int rk = __shfl_sync(FULL_MASK, req, k);
     const int ck = __shfl_sync(FULL_MASK, capk, k);
@@ -615,7 +668,7 @@ __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, ui
                                             const int* cap, int n, int m, int rs, uint32_t a_scr,
                                             uint32_t a_ord, int* __restrict__ starts_out) {
   const int lane = threadIdx.x & 31;
-  const uint32_t a_c = a_scr, a_cb = a_scr + 4 * m * rs, a_es = a_cb + 4 * rs;
+  const uint32_t a_c = a_scr, a_cb = a_scr + 4 * m * rs, a_es = a_cb + 4 * m * rs;
   for (int j = lane; j < m * rs; j += 32) sts32(a_c + 4 * j, 0);
   for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
