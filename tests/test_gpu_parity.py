@@ -481,7 +481,9 @@ def test_time_limited_solve_stops_on_the_device_clock():
     cfg = SolveConfig(total_iters=10 ** 7, workers=4, pool_size=8, tabu_size=800, delta=60,
                       phi_steps=20, phi_max=3, seed=1, time_limit_s=0.4)
     r = BatchSolver(insts, [1] * 6, cfg).run()
-    assert 0.3 < r.search_ms * 1e-3 < 1.0
+    assert r.search_ms * 1e-3 < 1.0
+    # it ran to the limit unless every instance reached the critical path first
+    assert r.search_ms * 1e-3 > 0.3 or (r.best_cmax == r.critical_path).all()
     assert (r.iterations < 10 ** 7).all()
     # an instance the pool already solved to the critical path never searches
     assert ((r.iterations > 0) | (r.best_cmax == r.critical_path)).all()
