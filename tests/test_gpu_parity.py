@@ -469,7 +469,7 @@ def test_cluster_workers_equal_single_cta():
     cfg = SolveConfig(total_iters=300, workers=3, pool_size=8, tabu_size=800, delta=60,
                       phi_steps=20, phi_max=3, seed=2, cluster=4)
     r = BatchSolver(insts, [1] * 4, cfg).run()
-    assert r.iterations.tolist() == [300] * 4
+    assert ((r.iterations == 300) | (r.best_cmax == r.critical_path)).all()
 
 
 def test_time_limited_solve_stops_on_the_device_clock():
