@@ -514,11 +514,14 @@ __host__ __device__ __forceinline__ int cap_warp_words(int n, int m, int rmax) {
 // Alg. 4 (kernels.py:81-110) on one resource row from entry i0 on, one
 // lane, quirks preserved.  Entries before i0 are the leading run with
 // c >= start + dur, which the reference's loop skips one by one.
+// (copy_idx0, effort0): resume after entries already processed (effort0 < 0:
+// the full effort req * dur, nothing processed yet)
 __device__ __forceinline__ void cap_commit_row(uint32_t a_c, uint32_t a_cb, int capk, int req,
-                                               int start, int dur, int i0 = 0) {
-  int effort = req * dur;
+                                               int start, int dur, int i0 = 0,
+                                               int copy_idx0 = 0, int effort0 = -1) {
+  int effort = effort0 < 0 ? req * dur : effort0;
   if (effort <= 0) return;
-  int copy_idx = 0, new_time = start + dur;
+  int copy_idx = copy_idx0, new_time = start + dur;
   for (int i = i0; effort > 0 && i < capk; ++i) {
     const int cv = static_cast<int>(lds32(a_c + 4 * i));
     if (cv < new_time) {
@@ -608,13 +611,35 @@ __device__ __forceinline__ void cap_commit_groups(uint32_t a_c, uint32_t a_cb, i
   const bool pr = j < hi - lo && static_cast<int>(lds32(row + 4 * (lo + j))) < T;
   const uint32_t b = (__ballot_sync(FULL_MASK, pr) >> (8 * g)) & 0xffu;
   const int i0 = b ? lo + __ffs(b) - 1 : capk;
-  if (act && i0 < capk) {
-    const int c0 = static_cast<int>(lds32(row + 4 * i0));
-    if (c0 <= start && i0 + req <= capk) {
-      for (int t = j; t < req; t += 8) sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
-    } else if (j == 0) {
-      cap_commit_row(row, cbrow, capk, req, start, dur, i0);
+  const bool has = act && i0 < capk;
+  const int c0 = has ? static_cast<int>(lds32(row + 4 * i0)) : 0;
+  const bool fast = has && c0 <= start && i0 + req <= capk;
+  // c0 > start: the reference's loop processes exactly the req entries from i0
+  // with new_time = start + dur before the effort can run out (the effort left
+  // after entry k is (req-k-1)*dur + sum (max(c, start) - start) > 0), so those
+  // steps run side by side; the loop resumes after them with copy_idx = req
+  // and the effort still left
+  const bool ph1 = has && !fast && i0 + req <= capk;
+  int part = 0;
+  if (fast) {
+    for (int t = j; t < req; t += 8) sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
+  } else if (ph1) {
+    for (int t = j; t < req; t += 8) {
+      const int cv = static_cast<int>(lds32(row + 4 * (i0 + t)));
+      sts32(cbrow + 4 * t, static_cast<uint32_t>(cv));
+      sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
+      part += max(cv, start) - start;
     }
+  }
+  part += __shfl_xor_sync(FULL_MASK, part, 1);  // group sums (all lanes take part)
+  part += __shfl_xor_sync(FULL_MASK, part, 2);
+  part += __shfl_xor_sync(FULL_MASK, part, 4);
+  __syncwarp();
+  if (j == 0) {
+    if (ph1)
+      cap_commit_row(row, cbrow, capk, req, start, dur, i0 + req, req, part);
+    else if (has && !fast)
+      cap_commit_row(row, cbrow, capk, req, start, dur, i0);
   }
   __syncwarp();
 }
