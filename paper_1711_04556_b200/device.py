@@ -412,6 +412,11 @@ def _raise_dev_err(err) -> None:
 
 @dataclass
 class SolveConfig:
+    """Everything one batch solve needs (the reference's SearchParams plus the
+    device choices).  Every device choice is result-neutral: evaluator groups,
+    prefix reuse, clusters and CTA sizes give the same makespans and, for one
+    worker per instance, the same trajectories."""
+
     total_iters: int
     workers: int
     pool_size: int
@@ -427,7 +432,7 @@ class SolveConfig:
     steal: bool = True        # B > 1: idle workers help instances with budget left
     full_sgs: bool = False    # True: no prefix reuse in the group-32 evaluators
     cap_group: int | None = None  # CAPACITY: 32 = warp, 1 = thread per schedule, None = auto
-    cluster: int | None = None    # CTAs per worker (1..8; TIME group 32), None = auto
+    cluster: int | None = None    # CTAs per worker (1..8, prefix-reusing evaluators), None = auto
     time_limit_s: float | None = None  # wall-clock budget of the search on the device clock
 
     @property
