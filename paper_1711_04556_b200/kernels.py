@@ -116,7 +116,7 @@ def tabu_add(tabu_list, tabu_count, head, u, v) -> int:
     """Circular-list insert with counter mirror (kernels.py:263-277).
 
     Host bookkeeping for TabuState snapshots; the device search keeps its own
-    shared-memory list (csrc/search.cuh:tabu_add1).
+    shared-memory list (csrc/cta.cuh:tabu_add1).
     """
     ou, ov = int(tabu_list[head, 0]), int(tabu_list[head, 1])
     if ou != 0 or ov != 0:
