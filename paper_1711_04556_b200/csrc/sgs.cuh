@@ -260,7 +260,13 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   const uint32_t r0 = static_cast<uint32_t>(rec.y);
   const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
   int start = esv;
-  if (dur > 0 && (r0 | r1) != 0) {
+  if constexpr (!BIG) {
+    // no branch on es < hw or on the demand: from hw on every slot is free, so
+    // the first round returns es; a zero demand or duration books nothing
+    start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                static_cast<uint32_t>(rec.w), err);
+    warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
+  } else if (dur > 0 && (r0 | r1) != 0) {
     if (esv < hw)
       start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
                                   static_cast<uint32_t>(rec.w), err);
