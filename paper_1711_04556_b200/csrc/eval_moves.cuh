@@ -133,7 +133,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (;;) {
       const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
       const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_pull<W, BIG>(act, rec, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
+      const int st = time_step_pull<W, BIG, false>(act, rec, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
                                             a_fin, hw, cm, err);
       log_below(act, rec, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
@@ -146,7 +146,9 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       ++p;
       act = act_n;
       rec = rec_n;
+      __syncwarp();  // after the loop test: the next REDUX follows it branch-free
     }
+    __syncwarp();
     // phase B, positions p..pend-1 after a divergence; unrolled by two so the
     // prefetched next activity needs no register copies
     if (div && p < pend) {
@@ -155,16 +157,18 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // ord[n]: pad
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_pull<W, BIG>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
+        int st = time_step_pull<W, BIG, false>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
                                           a_tau, a_fin, hw, cm, err);
         log_below(act_a, rec_a, st);
         if (++p >= pend) break;
+        __syncwarp();  // after the loop test: the next REDUX follows it branch-free
         act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_pull<W, BIG>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
+        st = time_step_pull<W, BIG, false>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
                                       a_fin, hw, cm, err);
         log_below(act_b, rec_b, st);
         if (++p >= pend) break;
+        __syncwarp();
       }
     }
     if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);

@@ -103,11 +103,9 @@ template <int W, bool HCHK>
 __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
                                                        uint32_t r0, uint32_t r1, uint32_t cap0,
                                                        uint32_t cap1, uint32_t hi) {
-  uint32_t w0 = cap0, w1 = cap1;
-  if (t < hw) {
-    w0 = lds32(a_tau + 4 * W * t);
-    if (W == 2) w1 = lds32(a_tau + 4 * W * t + 4);
-  }
+  const bool in = t < hw;
+  const uint32_t w0 = lds32_if(in, a_tau + 4 * W * t, cap0);
+  const uint32_t w1 = W == 2 ? lds32_if(in, a_tau + 4 * W * t + 4, cap1) : cap1;
   // HCHK = false (the SGS): no t < H test -- packing rejects demands above
   // capacity, so every activity fits from hw on (slots >= hw are free) and no
   // window reaches past hw + dur <= H; the scan loop keeps its t0 >= H guard.
@@ -241,7 +239,7 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
 // fin[pred] (kernels.py:177-182 computes es_prec exactly so), then the window
 // and the booking as time_step_warp; fin[act] is recorded.  rec is the
 // activity's pull record (info_r: duration, demand, predecessor span, mask).
-template <int W, bool BIG>
+template <int W, bool BIG, bool SYNC = true>
 __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t a_pdat,
                                               uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                               uint32_t hi, int H, uint32_t a_tau, uint32_t a_fin,
@@ -275,7 +273,9 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   const int fin = start + dur;
   cmax = max(cmax, fin);
   sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
-  __syncwarp();
+  // SYNC = false: the caller synchronises after its own bookkeeping, so the
+  // next step's REDUX needs no divergence check
+  if (SYNC) __syncwarp();
   return start;
 }
 
