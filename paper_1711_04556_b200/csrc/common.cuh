@@ -25,6 +25,9 @@ enum BlobField {
   B_HDR = 32
 };
 constexpr int BLOB_MAGIC = 0x52435053;  // "RCPS"
+// slots past the horizon H + 1 of the prefix-reusing TIME evaluator's profile:
+// a scan round starting at t <= H reads up to t + 31
+constexpr int TAU_PAD = 32;
 
 // error codes written to the device error word (first error wins)
 enum DevErr {

@@ -99,13 +99,17 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 // first t >= esv with [t, t+dur) fitting, slots >= hw at capacity, t+dur <= H.
 // Each round tests 32 slots and resolves the window branch-free: the run
 // carried from the previous round, else the first run of `dur` ones.
-template <int W, bool HCHK>
+// MAT: the profile is materialised at capacity from hw on (and 32 slots past
+// the horizon), so the load needs no test
+template <int W, bool HCHK, bool MAT = false>
 __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
                                                        uint32_t r0, uint32_t r1, uint32_t cap0,
                                                        uint32_t cap1, uint32_t hi) {
-  const bool in = t < hw;
-  const uint32_t w0 = lds32_if(in, a_tau + 4 * W * t, cap0);
-  const uint32_t w1 = W == 2 ? lds32_if(in, a_tau + 4 * W * t + 4, cap1) : cap1;
+  const bool in = MAT || t < hw;
+  const uint32_t w0 = MAT ? lds32(a_tau + 4 * W * t) : lds32_if(in, a_tau + 4 * W * t, cap0);
+  const uint32_t w1 = W == 2 ? (MAT ? lds32(a_tau + 4 * W * t + 4)
+                                    : lds32_if(in, a_tau + 4 * W * t + 4, cap1))
+                             : cap1;
   // HCHK = false (the SGS): no t < H test -- packing rejects demands above
   // capacity, so every activity fits from hw on (slots >= hw are free) and no
   // window reaches past hw + dur <= H; the scan loop keeps its t0 >= H guard.
@@ -118,7 +122,7 @@ __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, in
 // BIG = false (every duration <= 32): a lane whose window would end past the
 // round cannot hit -- m >> lane brings in zeros, and dmask covers them -- so
 // the candidate test is implied.
-template <int W, bool BIG = true, bool HCHK = false>
+template <int W, bool BIG = true, bool HCHK = false, bool MAT = false>
 __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32_t r0,
                                            uint32_t r1, uint32_t cap0, uint32_t cap1,
                                            uint32_t hi, int esv, int dur, uint32_t dmask,
@@ -129,7 +133,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   const bool cand = !BIG || lane + dur <= 32;
   // first round, peeled: nothing is carried in, so lane 0's test covers the
   // window starting at esv
-  uint32_t m = window_fits_ballot<W, HCHK>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
+  uint32_t m = window_fits_ballot<W, HCHK, MAT>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
   uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
   if (y) return esv + __ffs(y) - 1;
   int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
@@ -139,7 +143,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
       if (lane == 0) set_err(err, DE_NO_WINDOW);
       return H;
     }
-    m = window_fits_ballot<W, HCHK>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
+    m = window_fits_ballot<W, HCHK, MAT>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
     const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
     if (carry + tz >= dur) return t0 - carry;
     y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
@@ -181,6 +185,28 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
       if (W == 2) sts32(adr + 4, (old ? lds32(adr + 4) : cap1) - r1);
     }
   hw = max(hw, fin);
+}
+
+// warp_commit on a materialised profile (slots >= hw hold the capacity):
+// no gap to fill, every booked slot is a read-modify-write
+template <int W, bool BIG = true>
+__device__ __forceinline__ void warp_commit_mat(uint32_t a_tau, int& hw, int start, int dur,
+                                                uint32_t r0, uint32_t r1) {
+  const int lane = threadIdx.x & 31;
+  const int t = start + lane;
+  {
+    const uint32_t adr = a_tau + 4 * W * t;  // t < H + 32: inside the padded profile
+    const bool in = lane < dur;
+    sts32_if(in, adr, lds32(adr) - r0);
+    if (W == 2) sts32_if(in, adr + 4, lds32(adr + 4) - r1);
+  }
+  if (BIG && dur > 32)
+    for (int tt = t + 32; tt < start + dur; tt += 32) {
+      const uint32_t adr = a_tau + 4 * W * tt;
+      sts32(adr, lds32(adr) - r0);
+      if (W == 2) sts32(adr + 4, lds32(adr + 4) - r1);
+    }
+  hw = max(hw, start + dur);
 }
 
 // Inverse of warp_commit below the mark `hw_keep`: give the demand on
@@ -239,7 +265,7 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
 // fin[pred] (kernels.py:177-182 computes es_prec exactly so), then the window
 // and the booking as time_step_warp; fin[act] is recorded.  rec is the
 // activity's pull record (info_r: duration, demand, predecessor span, mask).
-template <int W, bool BIG, bool SYNC = true>
+template <int W, bool BIG, bool SYNC = true, bool MAT = false>
 __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t a_pdat,
                                               uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                               uint32_t hi, int H, uint32_t a_tau, uint32_t a_fin,
@@ -261,14 +287,20 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   if constexpr (!BIG) {
     // no branch on es < hw or on the demand: from hw on every slot is free, so
     // the first round returns es; a zero demand or duration books nothing
-    start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
-                                static_cast<uint32_t>(rec.w), err);
-    warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
+    start = warp_window<W, BIG, false, MAT>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                            static_cast<uint32_t>(rec.w), err);
+    if (MAT)
+      warp_commit_mat<W, BIG>(a_tau, hw, start, dur, r0, r1);
+    else
+      warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   } else if (dur > 0 && (r0 | r1) != 0) {
     if (esv < hw)
-      start = warp_window<W, BIG>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
-                                  static_cast<uint32_t>(rec.w), err);
-    warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
+      start = warp_window<W, BIG, false, MAT>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                              static_cast<uint32_t>(rec.w), err);
+    if (MAT)
+      warp_commit_mat<W, BIG>(a_tau, hw, start, dur, r0, r1);
+    else
+      warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
   cmax = max(cmax, fin);
