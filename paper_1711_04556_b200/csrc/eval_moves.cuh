@@ -84,9 +84,11 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   if (lane == 0) sts32(a_ord + 4 * n, 0u);
   // the profile is kept materialised: every slot from the high-water mark on
   // (and the 32-slot pad past the horizon the scan may read) holds the capacity
+  // (capacity with every packed lane's guard bit set, see window_fits_ballot)
+  const uint32_t capg0 = cap0 | hi, capg1 = cap1 | hi;
   for (int t = lane; t < H + 1 + TAU_PAD; t += 32) {
-    sts32(a_tau + 4 * W * t, cap0);
-    if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+    sts32(a_tau + 4 * W * t, capg0);
+    if (W == 2) sts32(a_tau + 4 * W * t + 4, capg1);
   }
   __syncwarp();
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
@@ -126,7 +128,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     // log the bookings below hw_pre for the undo
     // (entry: start << 16 | activity; horizons are < 2^16, see KEY_LIMIT)
     auto log_below = [&](int act, const int4& rec, int st) {
-      if (st < hw_pre && rec.x > 0) {
+      if (st < hw_pre && (!BIG || rec.x > 0)) {  // (a zero duration gives back nothing)
         if (lane == 0) sts64(a_log + 8 * nlog, (static_cast<uint32_t>(rec.x) << 16) | st,
                              W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act));
         ++nlog;
@@ -192,10 +194,11 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       warp_uncommit<W>(a_tau, hw_pre, static_cast<int>(ent.x & 0xffffu),
                        static_cast<int>(ent.x >> 16), r0, r1);
     }
-    // ... and give [hw_pre, hw) back its capacity
-    for (int t = hw_pre + lane; t < hw; t += 32) {
-      sts32(a_tau + 4 * W * t, cap0);
-      if (W == 2) sts32(a_tau + 4 * W * t + 4, cap1);
+    // ... and give [hw_pre, hw) back its capacity (!BIG: every step raises hw
+    // to its finish time, so cm >= hw bounds the range and hw is not kept)
+    for (int t = hw_pre + lane, e = BIG ? hw : cm; t < e; t += 32) {
+      sts32(a_tau + 4 * W * t, capg0);
+      if (W == 2) sts32(a_tau + 4 * W * t + 4, capg1);
     }
     __syncwarp();
   }

@@ -79,6 +79,14 @@ __device__ __forceinline__ void red_max_shared(uint32_t a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// a - b kept as one subtraction (the guard-bit test below then folds the
+// complement into its LOP3 instead of being rewritten as ~a + b)
+__device__ __forceinline__ uint32_t sub_opaque(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 // wrap-mode funnel shift: y >> (s & 31) (the window shift fields are 5 bits)
 __device__ __forceinline__ uint32_t shr_wrap(uint32_t y, int s) {
   return __funnelshift_r(y, 0u, static_cast<uint32_t>(s));
@@ -100,7 +108,9 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 // Each round tests 32 slots and resolves the window branch-free: the run
 // carried from the previous round, else the first run of `dur` ones.
 // MAT: the profile is materialised at capacity from hw on (and 32 slots past
-// the horizon), so the load needs no test
+// the horizon), so the load needs no test, and every packed lane carries its
+// guard bit (hi) set -- a fitting demand leaves it set, so the test is one
+// subtraction
 template <int W, bool HCHK, bool MAT = false>
 __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
                                                        uint32_t r0, uint32_t r1, uint32_t cap0,
@@ -115,6 +125,9 @@ __device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, in
   // window reaches past hw + dur <= H; the scan loop keeps its t0 >= H guard.
   // The single-step state operation (arbitrary states) keeps the test, as the
   // reference's scan stops at the horizon (kernels.py:127).
+  if (MAT)  // the materialised profile keeps every lane's guard bit set
+    return __ballot_sync(FULL_MASK, (!HCHK || t < H) && (~sub_opaque(w0, r0) & hi) == 0u &&
+                                        (W == 1 || (~sub_opaque(w1, r1) & hi) == 0u));
   return __ballot_sync(FULL_MASK, (!HCHK || t < H) && fits1(w0, r0, hi) &&
                                       (W == 1 || fits1(w1, r1, hi)));
 }
