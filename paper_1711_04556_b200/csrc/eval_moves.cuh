@@ -81,6 +81,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
                  a_tau = sa(ws), a_fin = sa(ws + (H + 1 + TAU_PAD) * W),
                  a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + 8 * n;
+  // the lane's base addresses of the profile and the predecessor lists
+  const uint32_t a_tau_l = opaque(a_tau + 4 * W * lane), a_pdat_l = opaque(a_pdat + 4 * lane);
   if (lane == 0) sts32(a_ord + 4 * n, 0u);
   // the profile is kept materialised: every slot from the high-water mark on
   // (and the 32-slot pad past the horizon the scan may read) holds the capacity
@@ -111,7 +113,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       const int s = static_cast<int>(lds32(a_bst + 4 * act));
       const uint32_t r0 = static_cast<uint32_t>(rec.y);
       const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
-      if (rec.x > 0 && (r0 | r1) != 0) warp_commit_mat<W, BIG>(a_tau, hw_pre, s, rec.x, r0, r1);
+      if (rec.x > 0 && (r0 | r1) != 0) warp_commit_mat<W, BIG>(a_tau_l, hw_pre, s, rec.x, r0, r1);
       const int fin = s + rec.x;
       cm_pre = max(cm_pre, fin);
       sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
@@ -142,8 +144,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     for (;;) {
       const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
       const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_pull<W, BIG, false, true>(act, rec, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
-                                            a_fin, hw, cm, err);
+      const int st = time_step_pull<W, BIG, false, true>(act, rec, a_pdat_l, a_req, cap0, cap1,
+                                                         hi, H, a_tau_l, a_fin, hw, cm, err);
       log_below(act, rec, st);
       div = st != static_cast<int>(lds32(a_bst + 4 * act));
       if (div || p == v) {
@@ -166,15 +168,15 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // ord[n]: pad
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat, a_req, cap0, cap1, hi, H,
-                                          a_tau, a_fin, hw, cm, err);
+        int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
+                                                     hi, H, a_tau_l, a_fin, hw, cm, err);
         log_below(act_a, rec_a, st);
         if (++p >= pend) break;
         __syncwarp();  // after the loop test: the next REDUX follows it branch-free
         act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat, a_req, cap0, cap1, hi, H, a_tau,
-                                      a_fin, hw, cm, err);
+        st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
+                                                 a_tau_l, a_fin, hw, cm, err);
         log_below(act_b, rec_b, st);
         if (++p >= pend) break;
         __syncwarp();

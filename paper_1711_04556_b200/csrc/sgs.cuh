@@ -87,6 +87,15 @@ __device__ __forceinline__ uint32_t sub_opaque(uint32_t a, uint32_t b) {
   return d;
 }
 
+// v through an opaque move: keeps a precomputed base address (e.g. profile +
+// 4 W lane) a single register the slot offsets are added to, instead of the
+// compiler re-distributing it into (t + lane) * 4 + profile
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // wrap-mode funnel shift: y >> (s & 31) (the window shift fields are 5 bits)
 __device__ __forceinline__ uint32_t shr_wrap(uint32_t y, int s) {
   return __funnelshift_r(y, 0u, static_cast<uint32_t>(s));
@@ -111,15 +120,17 @@ __device__ __forceinline__ uint32_t window_runs(uint32_t m, int sh) {
 // the horizon), so the load needs no test, and every packed lane carries its
 // guard bit (hi) set -- a fitting demand leaves it set, so the test is one
 // subtraction
+// Lane i tests slot t0 + i.  With MAT, a_tau is the lane's base address
+// (profile + 4 W lane), so a slot address is one multiply-add.
 template <int W, bool HCHK, bool MAT = false>
-__device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t, int hw, int H,
+__device__ __forceinline__ uint32_t window_fits_ballot(uint32_t a_tau, int t0, int hw, int H,
                                                        uint32_t r0, uint32_t r1, uint32_t cap0,
                                                        uint32_t cap1, uint32_t hi) {
+  const int t = t0 + static_cast<int>(threadIdx.x & 31);
   const bool in = MAT || t < hw;
-  const uint32_t w0 = MAT ? lds32(a_tau + 4 * W * t) : lds32_if(in, a_tau + 4 * W * t, cap0);
-  const uint32_t w1 = W == 2 ? (MAT ? lds32(a_tau + 4 * W * t + 4)
-                                    : lds32_if(in, a_tau + 4 * W * t + 4, cap1))
-                             : cap1;
+  const uint32_t adr = MAT ? a_tau + 4 * W * t0 : a_tau + 4 * W * t;
+  const uint32_t w0 = MAT ? lds32(adr) : lds32_if(in, adr, cap0);
+  const uint32_t w1 = W == 2 ? (MAT ? lds32(adr + 4) : lds32_if(in, adr + 4, cap1)) : cap1;
   // HCHK = false (the SGS): no t < H test -- packing rejects demands above
   // capacity, so every activity fits from hw on (slots >= hw are free) and no
   // window reaches past hw + dur <= H; the scan loop keeps its t0 >= H guard.
@@ -146,7 +157,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   const bool cand = !BIG || lane + dur <= 32;
   // first round, peeled: nothing is carried in, so lane 0's test covers the
   // window starting at esv
-  uint32_t m = window_fits_ballot<W, HCHK, MAT>(a_tau, esv + lane, hw, H, r0, r1, cap0, cap1, hi);
+  uint32_t m = window_fits_ballot<W, HCHK, MAT>(a_tau, esv, hw, H, r0, r1, cap0, cap1, hi);
   uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
   if (y) return esv + __ffs(y) - 1;
   int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
@@ -156,7 +167,7 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
       if (lane == 0) set_err(err, DE_NO_WINDOW);
       return H;
     }
-    m = window_fits_ballot<W, HCHK, MAT>(a_tau, t0 + lane, hw, H, r0, r1, cap0, cap1, hi);
+    m = window_fits_ballot<W, HCHK, MAT>(a_tau, t0, hw, H, r0, r1, cap0, cap1, hi);
     const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
     if (carry + tz >= dur) return t0 - carry;
     y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
@@ -201,21 +212,21 @@ __device__ __forceinline__ void warp_commit(uint32_t a_tau, int& hw, int start, 
 }
 
 // warp_commit on a materialised profile (slots >= hw hold the capacity):
-// no gap to fill, every booked slot is a read-modify-write
+// no gap to fill, every booked slot is a read-modify-write.  a_tau_l: the
+// lane's base address (profile + 4 W lane).
 template <int W, bool BIG = true>
-__device__ __forceinline__ void warp_commit_mat(uint32_t a_tau, int& hw, int start, int dur,
+__device__ __forceinline__ void warp_commit_mat(uint32_t a_tau_l, int& hw, int start, int dur,
                                                 uint32_t r0, uint32_t r1) {
   const int lane = threadIdx.x & 31;
-  const int t = start + lane;
   {
-    const uint32_t adr = a_tau + 4 * W * t;  // t < H + 32: inside the padded profile
+    const uint32_t adr = a_tau_l + 4 * W * start;  // start + lane < H + 32: inside the pad
     const bool in = lane < dur;
     sts32_if(in, adr, lds32(adr) - r0);
     if (W == 2) sts32_if(in, adr + 4, lds32(adr + 4) - r1);
   }
   if (BIG && dur > 32)
-    for (int tt = t + 32; tt < start + dur; tt += 32) {
-      const uint32_t adr = a_tau + 4 * W * tt;
+    for (int k = 32; k < dur - lane; k += 32) {
+      const uint32_t adr = a_tau_l + 4 * W * (start + k);
       sts32(adr, lds32(adr) - r0);
       if (W == 2) sts32(adr + 4, lds32(adr + 4) - r1);
     }
@@ -278,6 +289,8 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
 // fin[pred] (kernels.py:177-182 computes es_prec exactly so), then the window
 // and the booking as time_step_warp; fin[act] is recorded.  rec is the
 // activity's pull record (info_r: duration, demand, predecessor span, mask).
+// MAT: materialised profile (see window_fits_ballot); a_tau and a_pdat are
+// then the lane's base addresses (+ 4 W lane, + 4 lane).
 template <int W, bool BIG, bool SYNC = true, bool MAT = false>
 __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t a_pdat,
                                               uint32_t a_req, uint32_t cap0, uint32_t cap1,
@@ -286,12 +299,16 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   const int lane = threadIdx.x & 31;
   const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
   // the predecessor lists are padded by 32 entries (common.cuh): every lane
-  // loads, lanes past the span are masked
-  int f = static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + lane))));
-  f = lane < pc ? f : 0;
+  // loads, lanes past the span are masked (MAT: a_pdat is the lane's base)
+  // (MAT: the span's start as one PRMT, then one multiply-add for the address)
+  const uint32_t p0b = MAT ? __byte_perm(static_cast<uint32_t>(rec.z), 0u, 0x4410) : 0u;
+  int f = static_cast<int>(lds32(a_fin + 4 * lds32(MAT ? a_pdat + 4 * p0b : a_pdat + 4 * (p0 + lane))));
+  // lane < pc, as one compare of the record word with (lane + 1) << 16
+  f = (MAT ? static_cast<uint32_t>(rec.z) >= ((lane + 1u) << 16) : lane < pc) ? f : 0;
   if (BIG && pc > 32)
     for (int e = lane + 32; e < pc; e += 32)
-      f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
+      f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(MAT ? a_pdat + 4 * (p0 + e - lane)
+                                                              : a_pdat + 4 * (p0 + e)))));
   const int esv = __reduce_max_sync(FULL_MASK, f);
   const int dur = rec.x;
   const uint32_t r0 = static_cast<uint32_t>(rec.y);
