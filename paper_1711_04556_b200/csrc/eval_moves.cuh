@@ -186,6 +186,27 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     steps += p - u;  // converged: p = v + 1; else pend
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
+    if (!BIG) {
+      // one entry per lane (durations <= 32, a short serial loop each): the
+      // demand goes back by shared-memory additions, as entries may overlap
+      // in time -- no packed lane over- or underflows, since every partial
+      // sum lies between the booked and the restored value
+      for (int k0 = 0; k0 < nlog; k0 += 32) {
+        const int k = k0 + lane;
+        const uint2 ent = lds64(a_log + 8 * min(k, nlog - 1));
+        uint32_t r0 = ent.y, r1 = 0u;
+        if (W == 2) {
+          r0 = lds32(a_req + 8 * ent.y);
+          r1 = lds32(a_req + 8 * ent.y + 4);
+        }
+        const int s = static_cast<int>(ent.x & 0xffffu);
+        const int e = k < nlog ? min(s + static_cast<int>(ent.x >> 16), hw_pre) : s;
+        for (int t = s; t < e; ++t) {
+          red_add_shared(a_tau + 4 * W * t, r0);
+          if (W == 2) red_add_shared(a_tau + 4 * W * t + 4, r1);
+        }
+      }
+    } else
     for (int k = 0; k < nlog; ++k) {
       const uint2 ent = lds64(a_log + 8 * k);
       uint32_t r0 = ent.y, r1 = 0u;

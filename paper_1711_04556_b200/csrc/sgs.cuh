@@ -74,6 +74,10 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
 __device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
 }
+// *a += v as one shared-memory reduction (no return value)
+__device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 // es[s] = max(es[s], v) as one shared-memory reduction (no return value)
 __device__ __forceinline__ void red_max_shared(uint32_t a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
