@@ -128,11 +128,17 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
     // log the bookings below hw_pre for the undo
-    // (entry: start << 16 | activity; horizons are < 2^16, see KEY_LIMIT)
+    // (entry: dur << 16 | start, demand or activity; horizons are < 2^16, see
+    // KEY_LIMIT).  !BIG: every step is logged at its position, branch-free --
+    // the undo skips the bookings at or above hw_pre itself.
+    const uint32_t a_log_u = a_log - 8 * u;
     auto log_below = [&](int act, const int4& rec, int st) {
-      if (st < hw_pre && (!BIG || rec.x > 0)) {  // (a zero duration gives back nothing)
-        if (lane == 0) sts64(a_log + 8 * nlog, (static_cast<uint32_t>(rec.x) << 16) | st,
-                             W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act));
+      const uint32_t ex = (static_cast<uint32_t>(rec.x) << 16) | static_cast<uint32_t>(st),
+                     ey = W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act);
+      if (!BIG) {
+        sts64_if(lane == 0, a_log_u + 8 * p, ex, ey);
+      } else if (st < hw_pre && rec.x > 0) {  // (a zero duration gives back nothing)
+        if (lane == 0) sts64(a_log + 8 * nlog, ex, ey);
         ++nlog;
       }
     };
@@ -184,6 +190,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     }
     if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);
     steps += p - u;  // converged: p = v + 1; else pend
+    if (!BIG) nlog = p - u;
     // ---- undo the suffix's bookings below hw_pre
     __syncwarp();
     if (!BIG) {
