@@ -378,7 +378,7 @@ __device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_ev
 // swapped order; positions u_min..u-1 are the current order's, booked at their
 // known starts.
 //   per-warp scratch: L lanes x (c [m*R] | cb [R] | es [n]) interleaved by lane
-//                     | c_pre [m*rs] | cb_w [m*rs] | es_pre [n]
+//                     | c_pre [m*rs] | cb_w [rs] | es_pre [n]   (cap_prefix_words)
 __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_base, int o_bst,
                                                        int o_ctr, int o_evs,
                                                        const uint32_t* __restrict__ moves,
@@ -391,7 +391,7 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
   const int* bst = dsm + o_bst;
   int* st = dsm + o_evs + warp * warp_words;
   int* cpre = st + L * cap_thread_words(n, m, R);
-  int* esp = cpre + 2 * m * rs;
+  int* esp = cpre + (m + 1) * rs;
   const uint32_t a_cpre = sa(cpre), a_cbw = sa(cpre + m * rs), a_dem = sa(I.dem),
                  a_ctr = sa(dsm + o_ctr);
   const int capk = lane < m ? I.cap[lane] : 0;
@@ -422,7 +422,7 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
       const int dur = I.dur[act], s0 = bst[act];
       if (dur > 0) {
         const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
-        cap_commit_all(a_cpre, a_cbw, rs, m, capk, req, s0, dur);
+        cap_commit_seq(a_cpre, a_cbw, rs, m, capk, req, s0, dur);
       }
       const int fin = s0 + dur;
       cm_pre = max(cm_pre, fin);
@@ -614,7 +614,9 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
       // the current order's schedule (starts -> bst) on warp 0's prefix scratch
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       if (warp == 0) {
-        int* scr = c.evs + c.cap_lanes * cap_thread_words(c.I.n, c.I.m, c.I.rmax);
+        // (warp 0's whole scratch: the per-lane states are free between phases;
+        // eval_warp_words reserves cap_warp_words there)
+        int* scr = c.evs;
         sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
                      cap_row_stride(c.I.rmax), sa(scr), sa(c.base), c.bst);
         if (lane == 0) {

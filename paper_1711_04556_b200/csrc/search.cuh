@@ -149,7 +149,8 @@ __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, in
                                                int rmax, int cap_lanes) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + 4 * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
-  return cap_lanes * cap_thread_words(n, m, rmax) + cap_warp_words(n, m, rmax);
+  return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
+             cap_warp_words(n, m, rmax));
 }
 
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,

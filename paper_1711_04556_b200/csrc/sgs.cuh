@@ -586,6 +586,11 @@ __host__ __device__ __forceinline__ int cap_row_stride(int rmax) { return rmax |
 __host__ __device__ __forceinline__ int cap_warp_words(int n, int m, int rmax) {
   return 2 * m * cap_row_stride(rmax) + n;  // c rows | copy-buffer rows | es
 }
+// the thread-per-schedule evaluator's shared prefix: c rows | one copy-buffer
+// row | es (its updates run one resource after another, cap_commit_seq)
+__host__ __device__ __forceinline__ int cap_prefix_words(int n, int m, int rmax) {
+  return (m + 1) * cap_row_stride(rmax) + n;
+}
 
 // Alg. 4 (kernels.py:81-110) on one resource row from entry i0 on, one
 // lane, quirks preserved.  Entries before i0 are the leading run with
@@ -729,6 +734,17 @@ __device__ __forceinline__ void cap_commit_all(uint32_t a_c, uint32_t a_cb, int 
     cap_commit_groups(a_c, a_cb, rs, m, capk, req, start, dur);
     return;
   }
+  for (int k = 0; k < m; ++k) {
+    const int rk = __shfl_sync(FULL_MASK, req, k);
+    const int ck = __shfl_sync(FULL_MASK, capk, k);
+    cap_commit_warp(a_c + 4 * k * rs, a_cb, ck, rk, start, dur);
+  }
+}
+
+// The m resource updates one after another with the whole warp, sharing one
+// copy-buffer row (a_cb: rs words)
+__device__ __forceinline__ void cap_commit_seq(uint32_t a_c, uint32_t a_cb, int rs, int m,
+                                               int capk, int req, int start, int dur) {
   for (int k = 0; k < m; ++k) {
     const int rk = __shfl_sync(FULL_MASK, req, k);
     const int ck = __shfl_sync(FULL_MASK, capk, k);
