@@ -167,21 +167,31 @@ __device__ __forceinline__ int warp_window(uint32_t a_tau, int hw, int H, uint32
   // window starting at esv
   uint32_t m = window_fits_ballot<W, HCHK, MAT>(a_tau, esv, hw, H, r0, r1, cap0, cap1, hi);
   uint32_t y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
-  if (y) return esv + __ffs(y) - 1;
-  int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
-  for (;;) {
-    t0 += 32;
-    if (t0 >= H) {  // cannot happen for valid instances
-      if (lane == 0) set_err(err, DE_NO_WINDOW);
-      return H;
+  int start = esv + __ffs(y) - 1;  // (one branch on the first-round path)
+  if (y == 0u) {
+    int t0 = esv, carry = m == FULL_MASK ? 32 : __clz(~m);
+    for (;;) {
+      t0 += 32;
+      if (t0 >= H) {  // cannot happen for valid instances
+        if (lane == 0) set_err(err, DE_NO_WINDOW);
+        start = H;
+        break;
+      }
+      m = window_fits_ballot<W, HCHK, MAT>(a_tau, t0, hw, H, r0, r1, cap0, cap1, hi);
+      const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
+      if (carry + tz >= dur) {
+        start = t0 - carry;
+        break;
+      }
+      y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
+      if (y) {
+        start = t0 + __ffs(y) - 1;
+        break;
+      }
+      carry = tz == 32 ? carry + 32 : __clz(~m);
     }
-    m = window_fits_ballot<W, HCHK, MAT>(a_tau, t0, hw, H, r0, r1, cap0, cap1, hi);
-    const int tz = __popc(m & ~(m + 1u));  // fitting slots from t0 on (32: all)
-    if (carry + tz >= dur) return t0 - carry;
-    y = __ballot_sync(FULL_MASK, cand && (~(m >> lane) & dmask) == 0u);
-    if (y) return t0 + __ffs(y) - 1;
-    carry = tz == 32 ? carry + 32 : __clz(~m);
   }
+  return start;
 }
 
 // Book an activity on [start, start+dur) (kernels.py:139-146): materialise
