@@ -60,9 +60,11 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
 //   o_ctr: shared move counter (zeroed by the caller)
 //   per-warp scratch: tau (H+1)*W | fin [n] | log [2n] | ord [n + 1] (ord[n]: a
 //   valid pad the unrolled loop's prefetch may read)
-// The log lists the suffix bookings below hw_pre -- (start | dur << 16,
-// packed demand (W = 1) or activity (W = 2)) -- the only ones the undo has to
-// give back (a zero demand gives back nothing).
+// The undo gives back the suffix bookings below hw_pre (a zero demand gives
+// back nothing): with durations <= 32 every suffix step's booking is found
+// from ord, the records and fin, 32 at once; with longer ones (BIG) a log
+// lists them -- (start | dur << 16, packed demand (W = 1) or activity
+// (W = 2)) -- and the warp gives them back one by one.
 //   ctr_cl: != 0 -> the move counter (and the step counter after it) live in
 //   the cluster leader's shared memory at this shared::cluster address
 template <int W, bool BIG>
@@ -127,18 +129,15 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     __syncwarp();
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
-    // log the bookings below hw_pre for the undo
-    // (entry: dur << 16 | start, demand or activity; horizons are < 2^16, see
-    // KEY_LIMIT).  !BIG: every step is logged at its position, branch-free --
-    // the undo skips the bookings at or above hw_pre itself.
-    const uint32_t a_log_u = a_log - 8 * u;
+    // BIG: log the bookings below hw_pre for the undo (entry: dur << 16 |
+    // start, demand or activity; horizons are < 2^16, see KEY_LIMIT).  !BIG
+    // logs nothing: the undo finds every suffix step's booking from the
+    // order (ord[u..p)), the records and the finish times (fin).
     auto log_below = [&](int act, const int4& rec, int st) {
-      const uint32_t ex = (static_cast<uint32_t>(rec.x) << 16) | static_cast<uint32_t>(st),
-                     ey = W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act);
-      if (!BIG) {
-        sts64_if(lane == 0, a_log_u + 8 * p, ex, ey);
-      } else if (st < hw_pre && rec.x > 0) {  // (a zero duration gives back nothing)
-        if (lane == 0) sts64(a_log + 8 * nlog, ex, ey);
+      if (BIG && st < hw_pre && rec.x > 0) {  // (a zero duration gives back nothing)
+        if (lane == 0)
+          sts64(a_log + 8 * nlog, (static_cast<uint32_t>(rec.x) << 16) | static_cast<uint32_t>(st),
+                W == 1 ? static_cast<uint32_t>(rec.y) : static_cast<uint32_t>(act));
         ++nlog;
       }
     };
@@ -198,16 +197,16 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       // demand goes back by shared-memory additions, as entries may overlap
       // in time -- no packed lane over- or underflows, since every partial
       // sum lies between the booked and the restored value
+      // (position u + k's booking: start = fin - dur of its activity)
       for (int k0 = 0; k0 < nlog; k0 += 32) {
         const int k = k0 + lane;
-        const uint2 ent = lds64(a_log + 8 * min(k, nlog - 1));
-        uint32_t r0 = ent.y, r1 = 0u;
-        if (W == 2) {
-          r0 = lds32(a_req + 8 * ent.y);
-          r1 = lds32(a_req + 8 * ent.y + 4);
-        }
-        const int s = static_cast<int>(ent.x & 0xffffu);
-        const int e = k < nlog ? min(s + static_cast<int>(ent.x >> 16), hw_pre) : s;
+        const int a = static_cast<int>(lds32(a_ord + 4 * (u + min(k, nlog - 1))));
+        const int4 r = lds128(a_info + 16 * a);
+        const int f = static_cast<int>(lds32(a_fin + 4 * a));
+        uint32_t r0 = static_cast<uint32_t>(r.y), r1 = 0u;
+        if (W == 2) r1 = lds32(a_req + 8 * a + 4);
+        const int s = f - r.x;
+        const int e = k < nlog ? min(f, hw_pre) : s;
         for (int t = s; t < e; ++t) {
           red_add_shared(a_tau + 4 * W * t, r0);
           if (W == 2) red_add_shared(a_tau + 4 * W * t + 4, r1);
