@@ -170,21 +170,26 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     if (div && p < pend) {
       int act_a = act;
       int4 rec_a = rec;
-      for (;;) {
-        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // ord[n]: pad
+      // pairs while two positions remain (one loop test per pair), then one
+      for (; p + 1 < pend; p += 2) {
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
                                                      hi, H, a_tau_l, a_fin, hw, cm, err);
         log_below(act_a, rec_a, st);
-        if (++p >= pend) break;
-        __syncwarp();  // after the loop test: the next REDUX follows it branch-free
-        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
+        __syncwarp();
+        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 2)));  // ord[n]: pad
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
                                                  a_tau_l, a_fin, hw, cm, err);
         log_below(act_b, rec_b, st);
-        if (++p >= pend) break;
         __syncwarp();
+      }
+      if (p < pend) {
+        const int st = time_step_pull<W, BIG, false, true>(
+            act_a, rec_a, a_pdat_l, a_req, cap0, cap1, hi, H, a_tau_l, a_fin, hw, cm, err);
+        log_below(act_a, rec_a, st);
+        ++p;
       }
     }
     if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);
