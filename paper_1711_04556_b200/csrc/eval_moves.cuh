@@ -170,8 +170,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     if (div && p < pend) {
       int act_a = act;
       int4 rec_a = rec;
-      // pairs while two positions remain (one loop test per pair), then one
-      for (; p + 1 < pend; p += 2) {
+      // two steps (positions p, p + 1), the next activity prefetched
+      auto pair = [&]() {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
@@ -184,7 +184,15 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
                                                  a_tau_l, a_fin, hw, cm, err);
         log_below(act_b, rec_b, st);
         __syncwarp();
+        p += 2;
+      };
+      // one loop test per four positions (branches cost more than their
+      // instructions here), then a pair and a single step for the rest
+      while (p + 3 < pend) {
+        pair();
+        pair();
       }
+      if (p + 1 < pend) pair();
       if (p < pend) {
         const int st = time_step_pull<W, BIG, false, true>(
             act_a, rec_a, a_pdat_l, a_req, cap0, cap1, hi, H, a_tau_l, a_fin, hw, cm, err);
