@@ -144,25 +144,41 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     // phase A, positions u..v: until a start differs from the current
     // schedule's (then phase B) or v is reached with none differing
     // (converged: the rest is the current schedule)
+    // (unrolled by two like phase B, so the prefetched activity needs no
+    // register copies; p + 1 <= v + 1 < n)
     int act = static_cast<int>(lds32(a_ord + 4 * u));
     int4 rec = lds128(a_info + 16 * act);
-    for (;;) {
-      const int act_n = static_cast<int>(lds32(a_ord + 4 * (p + 1)));  // p + 1 <= v + 1 < n
-      const int4 rec_n = lds128(a_info + 16 * act_n);
-      const int st = time_step_pull<W, BIG, false, true>(act, rec, a_pdat_l, a_req, cap0, cap1,
-                                                         hi, H, a_tau_l, a_fin, hw, cm, err);
-      log_below(act, rec, st);
-      div = st != static_cast<int>(lds32(a_bst + 4 * act));
-      if (div || p == v) {
+    {
+      int act_a = act;
+      int4 rec_a = rec;
+      for (;;) {
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
+        const int4 rec_b = lds128(a_info + 16 * act_b);
+        int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
+                                                     hi, H, a_tau_l, a_fin, hw, cm, err);
+        log_below(act_a, rec_a, st);
+        div = st != static_cast<int>(lds32(a_bst + 4 * act_a));
         ++p;
-        act = act_n;
-        rec = rec_n;
-        break;
+        if (div || p > v) {
+          act = act_b;
+          rec = rec_b;
+          break;
+        }
+        __syncwarp();  // after the loop test: the next REDUX follows it branch-free
+        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
+        rec_a = lds128(a_info + 16 * act_a);
+        st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
+                                                 a_tau_l, a_fin, hw, cm, err);
+        log_below(act_b, rec_b, st);
+        div = st != static_cast<int>(lds32(a_bst + 4 * act_b));
+        ++p;
+        if (div || p > v) {
+          act = act_a;
+          rec = rec_a;
+          break;
+        }
+        __syncwarp();
       }
-      ++p;
-      act = act_n;
-      rec = rec_n;
-      __syncwarp();  // after the loop test: the next REDUX follows it branch-free
     }
     __syncwarp();
     // phase B, positions p..pend-1 after a divergence; unrolled by two so the
