@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 5
+#define RCPSP_ABI_VERSION 6
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -93,6 +93,10 @@ typedef struct RcpspSolveArgs {
                                  * and no further iterations once it is spent */
     int64_t *t0_ns;             /* [1] launch start (atomicMin of every CTA's
                                  * first clock read); host sets INT64_MAX */
+    int64_t big_any;            /* 1 = some instance has a duration or a
+                                 * fan-out/-in above 32 (blob header B_BIG);
+                                 * 0 lets the TIME evaluator's shared-memory
+                                 * plan leave out its undo log (ABI 6) */
 } RcpspSolveArgs;
 
 int rcpsp_abi_version(void);

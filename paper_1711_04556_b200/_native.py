@@ -19,7 +19,7 @@ LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
 # A/B measurements of kernel variants (tools/ab_bench.sh) point this at another build
 if os.environ.get("RCPSP_B200_LIB"):
     LIB_PATH = Path(os.environ["RCPSP_B200_LIB"])
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lib = None
 
@@ -51,6 +51,7 @@ class RcpspSolveArgs(ctypes.Structure):
         ("rmax_max", ctypes.c_int64), ("words", ctypes.c_int64), ("group", ctypes.c_int64),
         ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
         ("cluster", ctypes.c_int64), ("time_budget_ns", ctypes.c_int64), ("t0_ns", _vp),
+        ("big_any", ctypes.c_int64),
     ]
 
 

@@ -58,8 +58,8 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1)*W | fin [n] | log [2n] | ord [n + 1] (ord[n]: a
-//   valid pad the unrolled loop's prefetch may read)
+//   per-warp scratch: tau (H+1+TAU_PAD)*W | fin [n] | log [2n] (BIG only) |
+//   ord [n + 1] (ord[n]: a valid pad the unrolled loop's prefetch may read)
 // The undo gives back the suffix bookings below hw_pre (a zero demand gives
 // back nothing): with durations <= 32 every suffix step's booking is found
 // from ord, the records and fin, 32 at once; with longer ones (BIG) a log
@@ -82,7 +82,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
                  a_tau = sa(ws), a_fin = sa(ws + (H + 1 + TAU_PAD) * W),
-                 a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + 8 * n;
+                 a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + (BIG ? 8 * n : 0);
   // the lane's base addresses of the profile and the predecessor lists
   const uint32_t a_tau_l = opaque(a_tau + 4 * W * lane), a_pdat_l = opaque(a_pdat + 4 * lane);
   if (lane == 0) sts32(a_ord + 4 * n, 0u);

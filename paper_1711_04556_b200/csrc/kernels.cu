@@ -848,10 +848,10 @@ size_t smem_per_sm() {
 // memory fits `limit` bytes
 bool fit_plan_limit(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
                     int T, int want_threads, size_t limit, int min_threads, SmemPlan& p,
-                    int& threads) {
+                    int& threads, int big = 1) {
   for (threads = want_threads; threads >= min_threads; threads -= 32) {
     for (int lanes = 32; lanes >= (mode == MODE_CAPACITY && G == 1 ? 1 : 32); --lanes) {
-      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes);
+      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes, big);
       if (static_cast<size_t>(p.total) * 4 <= limit) return true;
     }
   }
@@ -876,25 +876,26 @@ int sm_count() {
 // searches progress at once (j30: 563 M vs ~400 M schedules/s with 8 x 128
 // threads per SM, j60: 354 M vs 311 M; j120: 2 x 512 stays best)
 bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
-                     int T, int want_threads, SmemPlan& p, int& threads, long long grid = 0) {
+                     int T, int want_threads, SmemPlan& p, int& threads, long long grid = 0,
+                     int big = 1) {
   if (want_threads == 0 && n <= 64 && grid > 0) {
     const long long sms = sm_count();
     for (int per_sm : {8, 4}) {
       if (grid < per_sm * sms) continue;
       const int nt = 1024 / per_sm;
       const size_t lim = smem_per_sm() / per_sm - 1024;
-      if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, nt, lim, nt, p, threads))
+      if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, nt, lim, nt, p, threads, big))
         return true;
     }
   }
   if (want_threads == 0) {
     const size_t half = smem_per_sm() / 2 - 1024;
-    if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, 512, half, 256, p, threads))
+    if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, 512, half, 256, p, threads, big))
       return true;
     want_threads = 512;
   }
   return fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, want_threads, smem_optin(), 32, p,
-                        threads);
+                        threads, big);
 }
 
 template <class Kern>
@@ -1095,7 +1096,7 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.h_max), static_cast<int>(A.e_max),
                          static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
                          static_cast<int>(A.tabu_size), threads, p, nt,
-                         static_cast<long long>(n_ids) * A.workers))
+                         static_cast<long long>(n_ids) * A.workers, A.big_any ? 1 : 0))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;

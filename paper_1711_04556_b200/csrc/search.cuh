@@ -145,9 +145,11 @@ struct SmemPlan {
   int warp_words, total, cap_lanes;
 };
 
+// big: some instance of the launch has a duration or fan-out above 32 -- only
+// then does the prefix-reusing TIME evaluator keep an undo log (2n words)
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
-                                               int rmax, int cap_lanes) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + 4 * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
+                                               int rmax, int cap_lanes, int big = 1) {
+  if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));
@@ -155,7 +157,7 @@ __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, in
 
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,
                                               int rmax, int delta, int T, int nwarps,
-                                              int cap_lanes = 32) {
+                                              int cap_lanes = 32, int big = 1) {
   SmemPlan p;
   auto a4 = [](int x) { return (x + 3) & ~3; };
   int off = 0;
@@ -173,7 +175,7 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.red = off; off += 72;
   p.scal = off; off += SC_WORDS;
   p.cap_lanes = cap_lanes;
-  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes));
+  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big));
   p.evs = off; off += p.warp_words * nwarps;
   p.total = off;
   return p;

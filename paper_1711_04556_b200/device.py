@@ -488,6 +488,7 @@ class BatchSolver:
         self.e_max = max(int(b[B_E]) for b in blobs)
         self.m_max = max(int(b[B_M]) for b in blobs)
         self.rmax_max = max(int(b[B_RMAX]) for b in blobs)
+        self.big_any = int(any(int(b[B_BIG]) for b in blobs))
         self.nbhd_max = max(1, max(neighborhood_size(int(b[B_N]), cfg.delta) for b in blobs))
         if self.nbhd_max >= KEY_LIMIT:
             raise UnsupportedInstance(f"neighbourhood of {self.nbhd_max} moves >= {KEY_LIMIT}")
@@ -594,6 +595,7 @@ class BatchSolver:
         a.cluster = (cfg.cluster if cfg.cluster is not None
                      else pick_cluster(n_group * cfg.workers))
         a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
+        a.big_any = self.big_any
         a.t0_ns = ptr(self.t0)
         return a
 
