@@ -52,6 +52,13 @@ struct Hdr {
 
 }  // namespace
 
+// k_solve's launch bound (2 CTAs per SM): the prefix-reusing TIME evaluator
+// runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120);
+// the other evaluators keep 16 warps at 64 registers (at 56 the CAPACITY
+// thread evaluator spills: -16 % on j120)
+constexpr int ksolve_threads(int mode, int G) { return mode == MODE_TIME && G == 32 ? 576 : 512; }
+constexpr int KSOLVE_THREADS_MAX = 576;
+
 // =========================================================================
 // K1: batch evaluation
 
@@ -534,7 +541,7 @@ __device__ __forceinline__ void add64(int64_t* p, long long v) {
 // so the batch finishes together; without it (the reference's fixed
 // worker-to-pool mapping, and exact B = 1 trajectories) it exits.
 template <int MODE, int G, int W>
-__global__ void __launch_bounds__(512, 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
+__global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
                                                   int n_ids, SmemPlan plan) {
   int* smem = dsm;
   const int B = static_cast<int>(A.workers);
@@ -890,7 +897,8 @@ bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rma
   }
   if (want_threads == 0) {
     const size_t half = smem_per_sm() / 2 - 1024;
-    if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, 512, half, 256, p, threads, big))
+    if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, ksolve_threads(mode, G), half,
+                       256, p, threads, big))
       return true;
     want_threads = 512;
   }
@@ -1085,11 +1093,15 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   if (n_ids <= 0) return 0;
   RcpspSolveArgs A = *args;
   const int threads = static_cast<int>(A.threads);
-  if (threads % 32 || threads < 0 || threads > 512) return fail("threads must be 0 (auto) or 32..512, x32");
+  if (threads % 32 || threads < 0 || threads > KSOLVE_THREADS_MAX)
+    return fail("threads must be 0 (auto) or 32.." + std::to_string(KSOLVE_THREADS_MAX) + ", x32");
   if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words), static_cast<int>(A.m_max),
                   [&]<int MODE, int G, int W>() -> int {
+    if (threads > ksolve_threads(MODE, G))
+      return fail("threads must be <= " + std::to_string(ksolve_threads(MODE, G)) +
+                  " for this evaluator");
     SmemPlan p;
     int nt;
     if (!fit_search_plan(MODE, G, static_cast<int>(A.words), static_cast<int>(A.n_max), static_cast<int>(A.m_max),
