@@ -9,15 +9,19 @@
  * worker/working-set loop of cooperation.orchestrate) with a CUDA launch for
  * sm_100a.  Conventions:
  *   - every pointer is caller-owned DEVICE memory unless stated otherwise;
- *   - all calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy);
+ *   - every device call is asynchronous on `stream` (a cudaStream_t, NULL =
+ *     legacy) and never synchronises: launch sizing uses the instance shape
+ *     the caller passes in (RcpspShape, from rcpsp_pack_instance's host blob
+ *     via rcpsp_blob_shape), and the kernels check it against the device
+ *     blob's header (mismatch -> DE_BAD_BLOB in the err word);
  *   - return 0 on success, <0 on a host-side error; rcpsp_last_error()
  *     returns a thread-local message.  Device-side invariant violations are
  *     written to the caller's `err` word (first error wins, see DevErr in
  *     csrc/common.cuh) and read back only when the caller syncs;
- *   - an instance is a packed int32 "blob" built by the host packer
- *     (paper_1711_04556_b200/device.py:pack_instance) from the reference's
- *     KernelArrays (instance.py:53-80); batches are blobs concatenated with
- *     an int64 offset table.
+ *   - an instance is a packed int32 "blob" built by rcpsp_pack_instance (host
+ *     code, below) from the reference's KernelArrays fields (instance.py:53-80);
+ *     the caller copies it to device memory; batches are blobs concatenated
+ *     with an int64 offset table.
  * No torch types appear here; the Python host passes tensor data_ptr()s.
  */
 #ifndef RCPSP_TABU_B200_H
@@ -29,7 +33,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 6
+#define RCPSP_ABI_VERSION 7
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -93,14 +97,56 @@ typedef struct RcpspSolveArgs {
                                  * and no further iterations once it is spent */
     int64_t *t0_ns;             /* [1] launch start (atomicMin of every CTA's
                                  * first clock read); host sets INT64_MAX */
-    int64_t big_any;            /* 1 = some instance has a duration or a
-                                 * fan-out/-in above 32 (blob header B_BIG);
-                                 * 0 lets the TIME evaluator's shared-memory
-                                 * plan leave out its undo log (ABI 6) */
+    int64_t no_big;             /* 1 = the caller guarantees that no instance
+                                 * of the launch has a duration or a fan-out/
+                                 * -in above 32 (RcpspShape.big == 0): the
+                                 * TIME evaluator's shared-memory plan then
+                                 * leaves out its undo log.  0 (the zero-
+                                 * initialised default) is always safe.  A
+                                 * violated guarantee is caught on the device
+                                 * (DE_SMEM) instead of corrupting memory. */
 } RcpspSolveArgs;
+
+/* Shape of one packed instance (the blob header), what the host needs to size
+ * a launch without reading device memory. */
+typedef struct RcpspShape {
+    int32_t n;          /* activities incl. the two dummies                  */
+    int32_t m;          /* renewable resources                               */
+    int32_t horizon;    /* sum of durations (TIME profile length - 1)        */
+    int32_t edges;      /* precedence edges                                  */
+    int32_t words;      /* TIME packing: words per slot (0 = CAPACITY only)  */
+    int32_t lane_bits;  /* 8 or 16 (0 with words == 0)                       */
+    int32_t rmax;       /* max capacity (>= 1)                               */
+    int32_t cpm;        /* critical-path length (the search's floor)         */
+    int32_t len;        /* blob length in int32 words                        */
+    int32_t big;        /* a duration or fan-out/-in above 32                */
+} RcpspShape;
 
 int rcpsp_abi_version(void);
 const char *rcpsp_last_error(void);
+
+/* ---- host-side instance packing (no CUDA calls; usable without a GPU) ----
+ * Inputs are the reference's KernelArrays fields (instance.py:53-80):
+ * durations [n], demands [n*m] row-major, capacities [m], predecessor and
+ * successor CSR (ptr [n+1], dat [e], ids ascending per activity), horizon =
+ * sum of durations.  Every pointer is HOST memory.
+ * rcpsp_blob_words: validated size of the blob in int32 words, or -1.
+ * rcpsp_pack_instance: writes the blob (csrc/common.cuh layout) into `blob`
+ *   (blob_words >= rcpsp_blob_words); 0 or -1 (rcpsp_pack_last_error()).
+ *   Replaces the reference's ProjectInstance -> KernelArrays step
+ *   (instance.py:95-120) as the input of every device entry point below;
+ *   the levels (instance.py:396-415) and the critical path (instance.py:
+ *   374-388) are computed here.
+ * rcpsp_blob_shape: the shape of a packed (host) blob, for the entry points. */
+int64_t rcpsp_blob_words(const int32_t *dur, const int32_t *dem, const int32_t *cap, int n, int m,
+                         const int32_t *pred_ptr, const int32_t *pred_dat,
+                         const int32_t *succ_ptr, const int32_t *succ_dat, int32_t horizon);
+int rcpsp_pack_instance(const int32_t *dur, const int32_t *dem, const int32_t *cap, int n, int m,
+                        const int32_t *pred_ptr, const int32_t *pred_dat,
+                        const int32_t *succ_ptr, const int32_t *succ_dat, int32_t horizon,
+                        int32_t *blob, int64_t blob_words);
+int rcpsp_blob_shape(const int32_t *blob, RcpspShape *shape);
+const char *rcpsp_pack_last_error(void);
 
 /* Device properties used for launch sizing: SM count, opt-in smem/CTA. */
 int rcpsp_device_info(int *sm_count, int *smem_optin, int *cc_major, int *cc_minor);
@@ -110,15 +156,16 @@ int rcpsp_device_info(int *sm_count, int *smem_optin, int *cc_major, int *cc_min
  * reverse != 0 evaluates the time-reversed project (successor lists used as
  * predecessor lists, evaluator.py:336-344).  cmax: [B]; starts: [B*n] or
  * NULL.  group: TIME lanes per schedule (32/16/8). */
-int rcpsp_eval_batch(const int32_t *blob, int mode, const int32_t *orders, int batch,
+int rcpsp_eval_batch(const int32_t *blob, const RcpspShape *shape, int mode, const int32_t *orders, int batch,
                      int reverse, int32_t *cmax, int32_t *starts, int group, int32_t *err,
                      void *stream);
 
 /* filter_moves (kernels.py:218-255) over the reduced neighbourhood with
  * distance cap `delta` for a batch of orders: out_moves [batch*nbhd_cap]
  * packed (u<<16)|v in lexicographic order, out_count [batch]. */
-int rcpsp_filter_batch(const int32_t *blob, const int32_t *orders, int batch, int delta,
-                       uint32_t *out_moves, int nbhd_cap, int32_t *out_count, void *stream);
+int rcpsp_filter_batch(const int32_t *blob, const RcpspShape *shape, const int32_t *orders,
+                       int batch, int delta, uint32_t *out_moves, int nbhd_cap,
+                       int32_t *out_count, int32_t *err, void *stream);
 
 /* run_chunk (kernels.py:316-385) for `batch` independent searches on one
  * instance; one CTA each.  In/out: orders [batch*n], tabu [batch*T] packed,
@@ -127,7 +174,7 @@ int rcpsp_filter_batch(const int32_t *blob, const int32_t *orders, int batch, in
  * stats [batch*8] = (iters, evals, improved, local_best, cur, head, forced, 0)
  * -- the reference's 7-tuple.  Tabu counters are rebuilt from the list
  * (tabu.py:52-60); list entries must satisfy v-u <= delta. */
-int rcpsp_run_chunk_batch(const int32_t *blob, int mode, int delta, int tabu_size, int batch,
+int rcpsp_run_chunk_batch(const int32_t *blob, const RcpspShape *shape, int mode, int delta, int tabu_size, int batch,
                           int32_t *orders, uint32_t *tabu, int32_t *heads, const int32_t *budget,
                           const int32_t *adopted, const int32_t *start_cmax,
                           const int32_t *best_known, int floor_cmax, int32_t *best_orders,
@@ -163,15 +210,15 @@ int rcpsp_export_elites(const RcpspSolveArgs *args, int32_t *elites, int32_t *el
 
 /* diversify (search.py:77-94) for a batch of orders with per-order PCG64
  * states (advanced in place). */
-int rcpsp_diversify_batch(const int32_t *blob, int32_t *orders, int batch, int phi_steps,
-                          uint64_t *rng, void *stream);
+int rcpsp_diversify_batch(const int32_t *blob, const RcpspShape *shape, int32_t *orders,
+                          int batch, int phi_steps, uint64_t *rng, int32_t *err, void *stream);
 
 /* Single-step resource-state operations on the reference's state layouts
  * (kernels.py:68-146 via evaluator.py:171-209): op 0 = cap_earliest_start,
  * 1 = cap_update (arg = start), 2 = time_earliest_start (arg = es_prec),
  * 3 = time_update (arg = start).  state: CAP int32 [m][R_max], TIME int32
  * [m][H+1] (updated in place); out[0] receives the earliest start. */
-int rcpsp_state_op(const int32_t *blob, int op, int32_t *state, int act, int arg, int32_t *out,
+int rcpsp_state_op(const int32_t *blob, const RcpspShape *shape, int op, int32_t *state, int act, int arg, int32_t *out,
                    int32_t *err, void *stream);
 
 /* Parity probes of the device RNG and Eq. 8 (assigned_iterations,

@@ -19,7 +19,7 @@ LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
 # A/B measurements of kernel variants (tools/ab_bench.sh) point this at another build
 if os.environ.get("RCPSP_B200_LIB"):
     LIB_PATH = Path(os.environ["RCPSP_B200_LIB"])
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _lib = None
 
@@ -51,27 +51,42 @@ class RcpspSolveArgs(ctypes.Structure):
         ("rmax_max", ctypes.c_int64), ("words", ctypes.c_int64), ("group", ctypes.c_int64),
         ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
         ("cluster", ctypes.c_int64), ("time_budget_ns", ctypes.c_int64), ("t0_ns", _vp),
-        ("big_any", ctypes.c_int64),
+        ("no_big", ctypes.c_int64),
     ]
 
+
+class RcpspShape(ctypes.Structure):
+    """ctypes mirror of `RcpspShape` (the packed blob's header fields)."""
+
+    _fields_ = [(name, ctypes.c_int32) for name in
+                ("n", "m", "horizon", "edges", "words", "lane_bits", "rmax", "cpm", "len", "big")]
+
+
+_SHP = ctypes.POINTER(RcpspShape)
 
 _SIGNATURES = {
     "rcpsp_abi_version": ([], _i),
     "rcpsp_last_error": ([], ctypes.c_char_p),
+    "rcpsp_pack_last_error": ([], ctypes.c_char_p),
+    "rcpsp_blob_words": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, ctypes.c_int32],
+                         ctypes.c_int64),
+    "rcpsp_pack_instance": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, ctypes.c_int32, _vp,
+                             ctypes.c_int64], _i),
+    "rcpsp_blob_shape": ([_vp, _SHP], _i),
     "rcpsp_device_info": ([_vp, _vp, _vp, _vp], _i),
-    "rcpsp_eval_batch": ([_vp, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _vp], _i),
-    "rcpsp_filter_batch": ([_vp, _vp, _i, _i, _vp, _i, _vp, _vp], _i),
-    "rcpsp_run_chunk_batch": ([_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp,
-                               _vp, _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp], _i),
+    "rcpsp_eval_batch": ([_vp, _SHP, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _vp], _i),
+    "rcpsp_filter_batch": ([_vp, _SHP, _vp, _i, _i, _vp, _i, _vp, _vp, _vp], _i),
+    "rcpsp_run_chunk_batch": ([_vp, _SHP, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i,
+                               _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp], _i),
     "rcpsp_pool_init": ([ctypes.POINTER(RcpspSolveArgs), _vp, _i, _i, _vp, _vp], _i),
     "rcpsp_solve": ([ctypes.POINTER(RcpspSolveArgs), _vp, _i, _i, _vp], _i),
     "rcpsp_merge_elites": ([ctypes.POINTER(RcpspSolveArgs), _vp, _vp, _i, _vp], _i),
     "rcpsp_export_elites": ([ctypes.POINTER(RcpspSolveArgs), _vp, _vp, _vp], _i),
-    "rcpsp_diversify_batch": ([_vp, _vp, _i, _i, _vp, _vp], _i),
+    "rcpsp_diversify_batch": ([_vp, _SHP, _vp, _i, _i, _vp, _vp, _vp], _i),
     "rcpsp_rng_probe": ([_vp, _vp, _i, _vp, _vp], _i),
     "rcpsp_eq8_probe": ([_vp, _i, _vp, _vp], _i),
     "rcpsp_smem_probe": ([_i, _i, _i, _vp, _vp], _i),
-    "rcpsp_state_op": ([_vp, _i, _vp, _i, _i, _vp, _vp, _vp], _i),
+    "rcpsp_state_op": ([_vp, _SHP, _i, _vp, _i, _i, _vp, _vp, _vp], _i),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -90,6 +105,18 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
     if L.rcpsp_abi_version() != ABI_VERSION:
         raise NativeLibraryError(f"{path}: ABI {L.rcpsp_abi_version()} != {ABI_VERSION}")
     return L
+
+
+_host_lib = None
+
+
+def host_lib() -> ctypes.CDLL:
+    """The library for its host-only entry points (instance packing): needs
+    the built .so but no GPU -- no kernel is launched through this handle."""
+    global _host_lib
+    if _host_lib is None:
+        _host_lib = _lib if _lib is not None else load_library()
+    return _host_lib
 
 
 def lib() -> ctypes.CDLL:

@@ -206,6 +206,9 @@ class RunStats:
     stop_reason: str
     critical_path: int
     traces: list[np.ndarray] = field(default_factory=list)
+    # device time (CUDA events) of pool init + search; wall_time is the host
+    # perf_counter span as in the reference (cooperation.py:254, 273)
+    device_ms: float = 0.0
 
 
 def choose_mode(instance: ProjectInstance, params: SearchParams, requested: str,
@@ -227,7 +230,7 @@ def choose_mode(instance: ProjectInstance, params: SearchParams, requested: str,
 
 
 def _finish(instance: ProjectInstance, res: device.BatchResult, i: int, params: SearchParams,
-            mode_name: str, wall: float) -> RunStats:
+            mode_name: str, wall: float, device_ms: float | None = None) -> RunStats:
     n = instance.n_activities
     best_order = res.best_order[i, :n].astype(np.int32)
     schedule = evaluate(best_order, instance, int(res.best_mode[i]))
@@ -244,7 +247,8 @@ def _finish(instance: ProjectInstance, res: device.BatchResult, i: int, params: 
         exchanges=int(res.exchanges[i]), diversifications=int(res.diversifications[i]),
         forced_tabu_picks=int(res.forced[i]), workers=params.workers, mode=mode_name,
         stop_reason="critical_path" if int(res.best_cmax[i]) <= floor else "budget",
-        critical_path=floor, traces=res.traces[i] if res.traces else [])
+        critical_path=floor, traces=res.traces[i] if res.traces else [],
+        device_ms=res.device_ms if device_ms is None else device_ms)
 
 
 def orchestrate(instance: ProjectInstance, params: SearchParams, mode: EvalMode | None = None,
@@ -268,7 +272,7 @@ def orchestrate(instance: ProjectInstance, params: SearchParams, mode: EvalMode 
     solver = device.BatchSolver([instance], [int(mode)],
                                 _solve_config(params, time_limit_s=time_limit_s))
     res = solver.run()
-    return _finish(instance, res, 0, params, EvalMode(mode).name, res.device_ms * 1e-3)
+    return _finish(instance, res, 0, params, EvalMode(mode).name, res.wall_s)
 
 
 def _orchestrate_dynamic(instance: ProjectInstance, params: SearchParams,
@@ -278,6 +282,7 @@ def _orchestrate_dynamic(instance: ProjectInstance, params: SearchParams,
     mode = ctl.mode_for(0)
     cfg = _solve_config(params, grant_cap=window)
     solver = device.BatchSolver([instance], [int(mode)], cfg)
+    tick = time.perf_counter()
     solver.upload()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -300,8 +305,9 @@ def _orchestrate_dynamic(instance: ProjectInstance, params: SearchParams,
             solver.d_ids = {k: solver.d_ids[old] for k, old in
                             zip(solver.groups, list(solver.d_ids))}
         ev0.record()
+    wall = time.perf_counter() - tick
     res = solver.collect(ms, ms)
-    return _finish(instance, res, 0, params, "dynamic", ms * 1e-3)
+    return _finish(instance, res, 0, params, "dynamic", wall)
 
 
 @dataclass
@@ -313,6 +319,7 @@ class BatchStats:
     device_seconds: float
     wall_seconds: float
     launches: int
+    solve_wall_seconds: float = 0.0   # host: upload + pool init + search (synced)
 
     @property
     def schedules_per_second(self) -> float:
@@ -341,10 +348,11 @@ def orchestrate_batch(instances: list[ProjectInstance], params: SearchParams,
     res = solver.run()
     wall = time.perf_counter() - tick
     dev_s = res.device_ms * 1e-3
-    runs = [_finish(x, res, i, params, EvalMode(int(modes[i])).name, dev_s)
+    # every instance ran concurrently over the same host wall span
+    runs = [_finish(x, res, i, params, EvalMode(int(modes[i])).name, res.wall_s)
             for i, x in enumerate(instances)]
     return BatchStats(runs=runs, evaluations=int(res.evaluations.sum()), device_seconds=dev_s,
-                      wall_seconds=wall, launches=res.n_launches)
+                      wall_seconds=wall, launches=res.n_launches, solve_wall_seconds=res.wall_s)
 
 
 def _critical_path(instance: ProjectInstance) -> int:

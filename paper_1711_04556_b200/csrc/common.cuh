@@ -108,7 +108,7 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
     const int* sp = blob + blob[B_OFF_SPTR];
     const int* pp = blob + blob[B_OFF_PPTR];
     for (int a = threadIdx.x; a < n; a += blockDim.x) {
-      const int d = bd[a], r = br[a * W], sh = static_cast<int>(window_mask(d));
+      const int d = bd[a], r = W ? br[a * W] : 0, sh = static_cast<int>(window_mask(d));
       inf[a] = make_int4(d, r, sp[a] | ((sp[a + 1] - sp[a]) << 16), sh);
       inf[n + a] = make_int4(d, r, pp[a] | ((pp[a + 1] - pp[a]) << 16), sh);
     }

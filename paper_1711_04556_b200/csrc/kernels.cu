@@ -52,6 +52,17 @@ struct Hdr {
 
 }  // namespace
 
+// The launch was sized from the caller's RcpspShape: the device blob must
+// carry the same header (else DE_BAD_BLOB and the CTA leaves before staging).
+__device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const RcpspShape& s,
+                                         int* err) {
+  const bool ok = blob[B_MAGIC] == BLOB_MAGIC && blob[B_N] == s.n && blob[B_M] == s.m &&
+                  blob[B_H] == s.horizon && blob[B_E] == s.edges && blob[B_W] == s.words &&
+                  blob[B_RMAX] == s.rmax;
+  if (!ok && threadIdx.x == 0) set_err(err, DE_BAD_BLOB);
+  return ok;
+}
+
 // k_solve's launch bound (2 CTAs per SM): the prefix-reusing TIME evaluator
 // runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120);
 // the other evaluators keep 16 warps at 64 registers (at 56 the CAPACITY
@@ -63,11 +74,12 @@ constexpr int KSOLVE_THREADS_MAX = 576;
 // K1: batch evaluation
 
 template <int MODE, int G, int W>
-__global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob,
+__global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob, RcpspShape sh,
                                                     const int* __restrict__ orders, int batch,
                                                     int reverse, int* __restrict__ cmax,
                                                     int* __restrict__ starts, int cap_lanes,
                                                     int* err) {
+  if (!shape_ok(blob, sh, err)) return;
   int* smem = dsm;
   SInst I;
   const int used = align4(stage_instance(blob, smem, I));
@@ -133,10 +145,11 @@ __global__ void __launch_bounds__(256) k_eval_batch(const int* __restrict__ blob
 
 template <int MODE, int G, int W>
 __global__ void __launch_bounds__(512, 2) k_run_chunk(
-    const int* __restrict__ blob, int delta, int T, int* orders, uint32_t* tabu, int* heads,
+    const int* __restrict__ blob, RcpspShape sh, int delta, int T, int* orders, uint32_t* tabu, int* heads,
     const int* budget, const int* adopted, const int* start_cmax, const int* best_known,
     int floor_cmax, int* best_orders, int* trace, int trace_cap, long long* stats,
     uint32_t* moves_buf, int* cmax_buf, int nbhd_max, SmemPlan plan, int* err, int C) {
+  if (!shape_ok(blob, sh, err)) return;
   int* smem = dsm;
   const int b = blockIdx.x / C;  // search index; C > 1: a cluster of CTAs per search
   CtaCtx c;
@@ -186,9 +199,11 @@ __global__ void __launch_bounds__(512, 2) k_run_chunk(
 // =========================================================================
 // filter / diversify / probes
 
-__global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ blob, const int* orders,
-                                                      int delta, uint32_t* out_moves, int nbhd_cap,
-                                                      int* out_count, SmemPlan plan) {
+__global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ blob, RcpspShape sh,
+                                                      const int* orders, int delta,
+                                                      uint32_t* out_moves, int nbhd_cap,
+                                                      int* out_count, SmemPlan plan, int* err) {
+  if (!shape_ok(blob, sh, err)) return;
   int* smem = dsm;
   const int b = blockIdx.x;
   CtaCtx c;
@@ -201,8 +216,10 @@ __global__ void __launch_bounds__(256) k_filter_batch(const int* __restrict__ bl
   if (threadIdx.x == 0) out_count[b] = k;
 }
 
-__global__ void __launch_bounds__(256) k_diversify(const int* __restrict__ blob, int* orders, int steps,
-                                                   uint64_t* rng_words, SmemPlan plan) {
+__global__ void __launch_bounds__(256) k_diversify(const int* __restrict__ blob, RcpspShape sh,
+                                                   int* orders, int steps, uint64_t* rng_words,
+                                                   SmemPlan plan, int* err) {
+  if (!shape_ok(blob, sh, err)) return;
   int* smem = dsm;
   const int b = blockIdx.x;
   CtaCtx c;
@@ -275,8 +292,9 @@ __global__ void __launch_bounds__(1024) k_smem_probe(int iters, int* sink) {
 enum StateOp { OP_CAP_ES = 0, OP_CAP_UPDATE = 1, OP_TIME_ES = 2, OP_TIME_UPDATE = 3 };
 
 template <int W>
-__global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, int op, int* state,
-                                                 int act, int arg, int* out, int* err) {
+__global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, RcpspShape sh, int op,
+                                                 int* state, int act, int arg, int* out, int* err) {
+  if (!shape_ok(blob, sh, err)) return;
   int* smem = dsm;
   SInst I;
   const int used = align4(stage_instance(blob, smem, I));
@@ -559,6 +577,12 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
             A.moves_buf + static_cast<size_t>(wkr) * A.nbhd_max,
             A.cmax_buf + static_cast<size_t>(wkr) * A.nbhd_max, A.err);
   c.inc = A.full_sgs == 0;
+  // the shared-memory plan leaves out the TIME undo log only on the caller's
+  // no_big guarantee: an instance that needs it stops the launch loudly
+  if (A.no_big && c.I.big) {
+    if (tid == 0) set_err(A.err, DE_SMEM);
+    return;
+  }
   if (A.time_budget_ns > 0) {
     c.budget_ns = A.time_budget_ns;
     c.t0_ns = reinterpret_cast<const long long*>(A.t0_ns);
@@ -692,6 +716,10 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
       stage_instance(A.blob + A.blob_off[iid], smem + plan.inst, c.I);
       if (tid == 0) c.scal[SC_IID] = iid;
       __syncthreads();
+      if (A.no_big && c.I.big) {  // see the launch-entry check
+        if (tid == 0) set_err(A.err, DE_SMEM);
+        break;
+      }
       cta_init_rows(c);
       continue;
     }
@@ -821,13 +849,15 @@ __global__ void k_merge_elites(RcpspSolveArgs A, const int* elites, const int* e
 
 namespace {
 
-int read_hdr(const int32_t* dblob, Hdr& h) {
-  int w[B_HDR];
-  if (cuda_check(cudaMemcpy(w, dblob, sizeof(w), cudaMemcpyDeviceToHost), "read blob header"))
-    return -1;
-  if (w[B_MAGIC] != BLOB_MAGIC) return fail("bad instance blob (magic)");
-  h.n = w[B_N]; h.m = w[B_M]; h.H = w[B_H]; h.e = w[B_E]; h.W = w[B_W]; h.lb = w[B_LB];
-  h.rmax = w[B_RMAX]; h.cpm = w[B_CPM];
+// launch shape from the caller's RcpspShape (no device read: every entry
+// point stays asynchronous on its stream)
+int shape_hdr(const RcpspShape* s, Hdr& h) {
+  if (s == nullptr) return fail("null RcpspShape");
+  if (s->n < 1 || s->m < 0 || s->horizon < 0 || s->edges < 0 || s->words < 0 || s->words > 2 ||
+      s->rmax < 1)
+    return fail("RcpspShape out of range (use rcpsp_blob_shape on the packed blob)");
+  h.n = s->n; h.m = s->m; h.H = s->horizon; h.e = s->edges; h.W = s->words; h.lb = s->lane_bits;
+  h.rmax = s->rmax; h.cpm = s->cpm;
   return 0;
 }
 
@@ -954,11 +984,13 @@ int rcpsp_device_info(int* sm_count, int* smem_optin, int* cc_major, int* cc_min
   return 0;
 }
 
-int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int batch, int reverse,
-                     int32_t* cmax, int32_t* starts, int group, int32_t* err, void* stream) {
+int rcpsp_eval_batch(const int32_t* blob, const RcpspShape* shape, int mode, const int32_t* orders,
+                     int batch, int reverse, int32_t* cmax, int32_t* starts, int group,
+                     int32_t* err, void* stream) {
   if (batch <= 0) return 0;
   Hdr h;
-  if (read_hdr(blob, h)) return -1;
+  if (shape_hdr(shape, h)) return -1;
+  const RcpspShape sh = *shape;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t limit = smem_optin();
   const size_t inst = (inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3;
@@ -982,25 +1014,26 @@ int rcpsp_eval_batch(const int32_t* blob, int mode, const int32_t* orders, int b
     const int blocks = (batch + per_block - 1) / per_block;
     auto k = k_eval_batch<MODE, G, W>;
     if (set_smem(k, words * 4)) return -1;
-    k<<<blocks, nw * 32, words * 4, s>>>(blob, orders, batch, reverse, cmax, starts, lanes, err);
+    k<<<blocks, nw * 32, words * 4, s>>>(blob, sh, orders, batch, reverse, cmax, starts, lanes, err);
     return launch_check("k_eval_batch");
   });
 }
 
-int rcpsp_filter_batch(const int32_t* blob, const int32_t* orders, int batch, int delta,
-                       uint32_t* out_moves, int nbhd_cap, int32_t* out_count, void* stream) {
+int rcpsp_filter_batch(const int32_t* blob, const RcpspShape* shape, const int32_t* orders,
+                       int batch, int delta, uint32_t* out_moves, int nbhd_cap,
+                       int32_t* out_count, int32_t* err, void* stream) {
   if (batch <= 0) return 0;
   Hdr h;
-  if (read_hdr(blob, h)) return -1;
+  if (shape_hdr(shape, h)) return -1;
   const int threads = 256;
   SmemPlan p = plan_smem(MODE_TIME, 32, h.W, h.n, h.m, 0, h.e, h.rmax, delta, 1, 0);
   if (set_smem(k_filter_batch, p.total * 4)) return -1;
   k_filter_batch<<<batch, threads, p.total * 4, static_cast<cudaStream_t>(stream)>>>(
-      blob, orders, delta, out_moves, nbhd_cap, out_count, p);
+      blob, *shape, orders, delta, out_moves, nbhd_cap, out_count, p, err);
   return launch_check("k_filter_batch");
 }
 
-int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_size, int batch,
+int rcpsp_run_chunk_batch(const int32_t* blob, const RcpspShape* shape, int mode, int delta, int tabu_size, int batch,
                           int32_t* orders, uint32_t* tabu, int32_t* heads, const int32_t* budget,
                           const int32_t* adopted, const int32_t* start_cmax,
                           const int32_t* best_known, int floor_cmax, int32_t* best_orders,
@@ -1010,7 +1043,8 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
   if (batch <= 0) return 0;
   if (tabu_size < 1) return fail("tabu_size must be >= 1");
   Hdr h;
-  if (read_hdr(blob, h)) return -1;
+  if (shape_hdr(shape, h)) return -1;
+  const RcpspShape sh = *shape;
   if (threads % 32 || threads < 32 || threads > 512) return fail("threads must be 32..512, x32");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, group, h.W, h.m, [&]<int MODE, int G, int W>() -> int {
@@ -1025,7 +1059,7 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
     const bool shared_counter = MODE == MODE_TIME ? G == 32 : (G == 32 || h.n >= 48);
     int C = shared_counter ? std::min(8, std::max(1, 2 * sm_count() / batch)) : 1;
     if (C == 1) {
-      k<<<batch, nt, p.total * 4, s>>>(blob, delta, tabu_size, orders, tabu, heads, budget,
+      k<<<batch, nt, p.total * 4, s>>>(blob, sh, delta, tabu_size, orders, tabu, heads, budget,
                                             adopted, start_cmax, best_known, floor_cmax,
                                             best_orders, trace, trace_cap,
                                             reinterpret_cast<long long*>(stats), moves_buf,
@@ -1044,7 +1078,7 @@ int rcpsp_run_chunk_batch(const int32_t* blob, int mode, int delta, int tabu_siz
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cuda_check(cudaLaunchKernelEx(&cfg, k, blob, delta, tabu_size, orders, tabu, heads, budget,
+    if (cuda_check(cudaLaunchKernelEx(&cfg, k, blob, sh, delta, tabu_size, orders, tabu, heads, budget,
                                       adopted, start_cmax, best_known, floor_cmax, best_orders,
                                       trace, trace_cap, reinterpret_cast<long long*>(stats),
                                       moves_buf, cmax_buf, nbhd_max, p, err, C),
@@ -1108,7 +1142,7 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.h_max), static_cast<int>(A.e_max),
                          static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
                          static_cast<int>(A.tabu_size), threads, p, nt,
-                         static_cast<long long>(n_ids) * A.workers, A.big_any ? 1 : 0))
+                         static_cast<long long>(n_ids) * A.workers, A.no_big ? 0 : 1))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
@@ -1158,15 +1192,15 @@ int rcpsp_merge_elites(const RcpspSolveArgs* args, const int32_t* elites,
   return launch_check("k_merge_elites");
 }
 
-int rcpsp_diversify_batch(const int32_t* blob, int32_t* orders, int batch, int phi_steps,
-                          uint64_t* rng, void* stream) {
+int rcpsp_diversify_batch(const int32_t* blob, const RcpspShape* shape, int32_t* orders,
+                          int batch, int phi_steps, uint64_t* rng, int32_t* err, void* stream) {
   if (batch <= 0) return 0;
   Hdr h;
-  if (read_hdr(blob, h)) return -1;
+  if (shape_hdr(shape, h)) return -1;
   SmemPlan p = plan_smem(MODE_TIME, 32, h.W, h.n, h.m, 0, h.e, h.rmax, 1, 1, 0);
   if (set_smem(k_diversify, p.total * 4)) return -1;
   k_diversify<<<batch, 256, p.total * 4, static_cast<cudaStream_t>(stream)>>>(
-      blob, orders, phi_steps, rng, p);
+      blob, *shape, orders, phi_steps, rng, p, err);
   return launch_check("k_diversify");
 }
 
@@ -1175,21 +1209,22 @@ int rcpsp_smem_probe(int blocks, int threads, int iters, int32_t* sink, void* st
   return launch_check("k_smem_probe");
 }
 
-int rcpsp_state_op(const int32_t* blob, int op, int32_t* state, int act, int arg, int32_t* out,
-                   int32_t* err, void* stream) {
+int rcpsp_state_op(const int32_t* blob, const RcpspShape* shape, int op, int32_t* state, int act,
+                   int arg, int32_t* out, int32_t* err, void* stream) {
   Hdr h;
-  if (read_hdr(blob, h)) return -1;
+  if (shape_hdr(shape, h)) return -1;
   if (op < OP_CAP_ES || op > OP_TIME_UPDATE) return fail("unknown state op");
+  if (op >= OP_TIME_ES && h.W == 0) return fail("instance has no TIME packing (CAPACITY only)");
   if (act < 0 || act >= h.n) return fail("activity out of range");
   const size_t words = ((inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3) +
                        static_cast<size_t>(std::max((h.H + 1) * h.W, h.rmax)) + 4;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (h.W == 2) {
     if (set_smem(k_state_op<2>, words * 4)) return -1;
-    k_state_op<2><<<1, 32, words * 4, s>>>(blob, op, state, act, arg, out, err);
+    k_state_op<2><<<1, 32, words * 4, s>>>(blob, *shape, op, state, act, arg, out, err);
   } else {
     if (set_smem(k_state_op<1>, words * 4)) return -1;
-    k_state_op<1><<<1, 32, words * 4, s>>>(blob, op, state, act, arg, out, err);
+    k_state_op<1><<<1, 32, words * 4, s>>>(blob, *shape, op, state, act, arg, out, err);
   }
   return launch_check("k_state_op");
 }

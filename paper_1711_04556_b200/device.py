@@ -14,14 +14,16 @@ slot uses the same packing, so the per-slot window test is one word op.
 
 from __future__ import annotations
 
+import ctypes
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native
-from ._native import RcpspSolveArgs, check, ptr, stream_handle
-from .instance import ProjectInstance, compute_levels, critical_path_length
+from ._native import RcpspShape, RcpspSolveArgs, check, ptr, stream_handle
+from .instance import ProjectInstance
 
 MODE_CAPACITY = 0
 MODE_TIME = 1
@@ -45,77 +47,63 @@ class UnsupportedInstance(ValueError):
 
 
 def packing_for(capacities: np.ndarray) -> tuple[int, int]:
-    """(lane_bits, words per slot) of the TIME profile for these capacities."""
+    """(lane_bits, words per slot) of the TIME profile for these capacities,
+    (0, 0) when they do not pack into <= 2 words (CAPACITY mode only) --
+    the rule rcpsp_pack_instance applies (csrc/pack.cpp)."""
     cmax = int(np.max(capacities)) if len(capacities) else 0
-    if cmax <= 127:
-        lb = 8
-    elif cmax <= 32767:
-        lb = 16
-    else:
-        raise UnsupportedInstance(f"capacity {cmax} exceeds 32767")
-    words = max(1, math.ceil(len(capacities) / (32 // lb)))
-    if words > 2:
-        raise UnsupportedInstance(f"{len(capacities)} resources with {lb}-bit lanes need "
-                                  f"{words} words per slot (max 2)")
-    return lb, words
+    if not len(capacities):
+        return 8, 1
+    if cmax > 32767:
+        return 0, 0
+    lb = 8 if cmax <= 127 else 16
+    words = math.ceil(len(capacities) / (32 // lb))
+    return (lb, words) if words <= 2 else (0, 0)
+
+
+def _c_arrays(inst: ProjectInstance):
+    ka = inst.kernel_arrays
+    n, m = inst.n_activities, inst.n_resources
+    arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+            for a in (ka.durations, ka.demands, ka.capacities, ka.pred_ptr, ka.pred_dat,
+                      ka.succ_ptr, ka.succ_dat)]
+    return n, m, arrs, int(ka.horizon)
 
 
 def pack_instance(inst: ProjectInstance) -> np.ndarray:
-    """int32 blob of one instance (layout in the module docstring)."""
-    ka = inst.kernel_arrays
-    n, m = inst.n_activities, inst.n_resources
-    dur = np.asarray(ka.durations, np.int32)
-    dem = np.asarray(ka.demands, np.int32).reshape(n, m)
-    cap = np.asarray(ka.capacities, np.int32)
-    if (dur < 0).any():
-        raise ValueError("negative duration")
-    if (dem < 0).any():
-        raise ValueError("negative demand")
-    if m and (dem > cap[None, :]).any():
-        i, k = map(int, np.argwhere(dem > cap[None, :])[0])
-        raise ValueError(f"activity {i} demands {int(dem[i, k])} of resource {k} "
-                         f"with capacity {int(cap[k])}")
-    horizon = int(ka.horizon)
-    if horizon >= KEY_LIMIT - 1:
-        raise UnsupportedInstance(f"horizon {horizon} >= {KEY_LIMIT - 1}")
+    """int32 blob of one instance, built by the C ABI's host packer
+    (rcpsp_blob_words + rcpsp_pack_instance, csrc/pack.cpp; layout in the
+    module docstring).  Needs the built library but no GPU."""
+    L = _native.host_lib()
+    n, m, arrs, horizon = _c_arrays(inst)
     if n >= KEY_LIMIT:
         raise UnsupportedInstance(f"{n} activities >= {KEY_LIMIT}")
-    lb, W = packing_for(cap) if m else (8, 1)
-    lanes = 32 // lb
-    req = np.zeros((n, W), np.uint32)
-    capw = np.zeros(W, np.uint32)
-    for k in range(m):
-        w, sh = divmod(k, lanes)
-        req[:, w] |= dem[:, k].astype(np.uint32) << np.uint32(sh * lb)
-        capw[w] |= np.uint32(int(cap[k]) << (sh * lb))
-    levels = compute_levels(inst)
-    lptr = np.zeros(len(levels) + 1, np.int32)
-    lptr[1:] = np.cumsum([len(lv) for lv in levels])
-    ldat = np.array([a for lv in levels for a in lv], np.int32)
-    parts = [dur, dem.reshape(-1), cap, ka.pred_ptr, ka.pred_dat, ka.succ_ptr, ka.succ_dat,
-             req.reshape(-1).view(np.int32), capw.view(np.int32), lptr, ldat]
-    hdr = np.zeros(HDR, np.int32)
-    off = HDR
-    for slot, arr in zip(range(B_OFF_DUR, B_OFF_LDAT + 1), parts):
-        hdr[slot] = off
-        off += len(arr)
-    hdr[B_MAGIC] = BLOB_MAGIC
-    hdr[B_N], hdr[B_M], hdr[B_H], hdr[B_E] = n, m, horizon, len(ka.pred_dat)
-    hdr[B_W], hdr[B_LB] = W, lb
-    hdr[B_RMAX] = max(1, int(cap.max()) if m else 1)
-    hdr[B_CPM] = critical_path_length(inst)
-    hdr[B_LEN] = off
-    hdr[B_NLVL] = len(levels)
-    # 1 when a duration, a fan-out or a fan-in exceeds one warp (32): the
-    # search evaluator's multi-round booking / pull paths are compiled out
-    # otherwise.  The zero-duration sink (last activity) is never scheduled by
-    # it, so its fan-in does not count.
-    sink_free = int(inst.durations[n - 1]) == 0
-    fan = max([len(x) for x in inst.successors]
-              + [len(x) for i, x in enumerate(inst.predecessors)
-                 if not (sink_free and i == n - 1)] + [0])
-    hdr[B_BIG] = int(max(int(d) for d in inst.durations) > 32 or fan > 32)
-    return np.concatenate([hdr] + [np.asarray(p, np.int32) for p in parts])
+    if horizon >= KEY_LIMIT - 1:
+        raise UnsupportedInstance(f"horizon {horizon} >= {KEY_LIMIT - 1}")
+    dur, dem, cap, pp, pd, sp, sd = (a.ctypes.data for a in arrs)
+    words = L.rcpsp_blob_words(dur, dem, cap, n, m, pp, pd, sp, sd, horizon)
+    if words < 0:
+        raise ValueError(L.rcpsp_pack_last_error().decode(errors="replace"))
+    blob = np.zeros(int(words), dtype=np.int32)
+    if L.rcpsp_pack_instance(dur, dem, cap, n, m, pp, pd, sp, sd, horizon, blob.ctypes.data,
+                             int(words)) != 0:
+        raise ValueError(L.rcpsp_pack_last_error().decode(errors="replace"))
+    return blob
+
+
+def blob_shape(blob: np.ndarray) -> RcpspShape:
+    """RcpspShape of a packed host blob (rcpsp_blob_shape)."""
+    shape = RcpspShape()
+    blob = np.ascontiguousarray(blob, dtype=np.int32)
+    if _native.host_lib().rcpsp_blob_shape(blob.ctypes.data, ctypes.byref(shape)) != 0:
+        raise ValueError(_native.host_lib().rcpsp_pack_last_error().decode(errors="replace"))
+    return shape
+
+
+def require_time_packing(blob: np.ndarray, mode: int) -> None:
+    if int(mode) == MODE_TIME and int(blob[B_W]) == 0:
+        raise UnsupportedInstance(
+            "capacities / resource count do not fit the packed TIME profile (<= 8 resources "
+            "with capacities <= 127, <= 4 with <= 32767): use CAPACITY mode")
 
 
 def neighborhood_size(n: int, delta: int) -> int:
@@ -156,6 +144,7 @@ class DeviceInstance:
     inst: ProjectInstance
     blob_host: np.ndarray
     blob: object  # torch int32 cuda tensor
+    shape: RcpspShape = None
 
     @property
     def n(self) -> int:
@@ -177,7 +166,7 @@ def device_instance(inst: ProjectInstance) -> DeviceInstance:
     if hit is not None and hit.inst is inst:
         return hit
     host = pack_instance(inst)
-    dev = DeviceInstance(inst, host, to_dev(host))
+    dev = DeviceInstance(inst, host, to_dev(host), blob_shape(host))
     if len(_cache) > 256:
         _cache.clear()
     _cache[key] = dev
@@ -221,6 +210,7 @@ def eval_batch(inst: ProjectInstance, orders: np.ndarray, mode: int, reverse: bo
     torch = _torch()
     L = _native.lib()
     di = device_instance(inst)
+    require_time_packing(di.blob_host, mode)
     orders = np.ascontiguousarray(np.atleast_2d(orders), dtype=np.int32)
     B, n = orders.shape
     if n != di.n:
@@ -229,7 +219,7 @@ def eval_batch(inst: ProjectInstance, orders: np.ndarray, mode: int, reverse: bo
     cmax = torch.zeros(B, dtype=torch.int32, device="cuda")
     starts = torch.zeros((B, n), dtype=torch.int32, device="cuda") if want_starts else None
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    check(L.rcpsp_eval_batch(ptr(di.blob), int(mode), ptr(d_ord), B, int(bool(reverse)),
+    check(L.rcpsp_eval_batch(ptr(di.blob), ctypes.byref(di.shape), int(mode), ptr(d_ord), B, int(bool(reverse)),
                              ptr(cmax), ptr(starts), int(group), ptr(err), stream_handle()),
           "rcpsp_eval_batch")
     _raise_dev_err(err)
@@ -246,8 +236,11 @@ def filter_batch(inst: ProjectInstance, orders: np.ndarray, delta: int) -> list[
     cap = max(1, neighborhood_size(di.n, delta))
     out = torch.zeros((B, cap), dtype=torch.int32, device="cuda")
     cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
-    check(L.rcpsp_filter_batch(ptr(di.blob), ptr(to_dev(orders)), B, int(delta), ptr(out), cap,
-                               ptr(cnt), stream_handle()), "rcpsp_filter_batch")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    check(L.rcpsp_filter_batch(ptr(di.blob), ctypes.byref(di.shape), ptr(to_dev(orders)), B,
+                               int(delta), ptr(out), cap, ptr(cnt), ptr(err), stream_handle()),
+          "rcpsp_filter_batch")
+    _raise_dev_err(err)
     packed = out.cpu().numpy().view(np.uint32)
     res = []
     for b, k in enumerate(cnt.cpu().numpy()):
@@ -269,6 +262,7 @@ def run_chunk_batch(inst: ProjectInstance, mode: int, delta: int, orders, tabu_l
     torch = _torch()
     L = _native.lib()
     di = device_instance(inst)
+    require_time_packing(di.blob_host, mode)
     orders = np.ascontiguousarray(np.atleast_2d(orders), np.int32)
     S, n = orders.shape
     tl = np.stack([pack_moves(t) for t in tabu_lists]).astype(np.uint32)
@@ -293,7 +287,7 @@ def run_chunk_batch(inst: ProjectInstance, mode: int, delta: int, orders, tabu_l
         g = pick_cap_group(n, len(inst.capacities), max(int(c) for c in inst.capacities))
     else:
         g = pick_group(n)
-    check(L.rcpsp_run_chunk_batch(ptr(di.blob), int(mode), int(delta), T, S, ptr(d_ord),
+    check(L.rcpsp_run_chunk_batch(ptr(di.blob), ctypes.byref(di.shape), int(mode), int(delta), T, S, ptr(d_ord),
                                   ptr(d_tabu), ptr(d_head), *(ptr(v) for v in vecs),
                                   int(floor_cmax), ptr(best), ptr(trace), tcap, ptr(stats),
                                   ptr(mbuf), ptr(cbuf), nb, int(g), int(threads), ptr(err),
@@ -325,8 +319,11 @@ def diversify_batch(inst: ProjectInstance, orders, phi_steps: int, rng_states: n
     orders = np.ascontiguousarray(np.atleast_2d(orders), np.int32)
     d_ord = to_dev(orders)
     d_rng = to_dev(np.ascontiguousarray(rng_states, np.uint64).view(np.int64))
-    check(L.rcpsp_diversify_batch(ptr(di.blob), ptr(d_ord), orders.shape[0], int(phi_steps),
-                                  ptr(d_rng), stream_handle()), "rcpsp_diversify_batch")
+    err = _torch().zeros(1, dtype=_torch().int32, device="cuda")
+    check(L.rcpsp_diversify_batch(ptr(di.blob), ctypes.byref(di.shape), ptr(d_ord),
+                                  orders.shape[0], int(phi_steps), ptr(d_rng), ptr(err),
+                                  stream_handle()), "rcpsp_diversify_batch")
+    _raise_dev_err(err)
     rng_states[...] = d_rng.cpu().numpy().view(np.uint64).reshape(rng_states.shape)
     return d_ord.cpu().numpy()
 
@@ -367,7 +364,7 @@ def state_op(inst: ProjectInstance, op: str, state: np.ndarray, act: int, arg: i
     d_state = to_dev(np.ascontiguousarray(state, np.int32))
     out = torch.zeros(1, dtype=torch.int32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    check(L.rcpsp_state_op(ptr(di.blob), STATE_OPS[op], ptr(d_state), int(act), int(arg),
+    check(L.rcpsp_state_op(ptr(di.blob), ctypes.byref(di.shape), STATE_OPS[op], ptr(d_state), int(act), int(arg),
                            ptr(out), ptr(err), stream_handle()), "rcpsp_state_op")
     if int(err.cpu()[0]):
         raise ValueError("resource state holds values outside the packed lane range")
@@ -459,6 +456,7 @@ class BatchResult:
     traces: list = field(default_factory=list)   # per instance: list of chunk arrays
     n_launches: int = 0
     sgs_steps: int = 0               # activity steps the workers' neighbourhood SGS ran
+    wall_s: float = 0.0              # host perf_counter: upload + pool init + search (synced)
 
 
 class BatchSolver:
@@ -478,6 +476,8 @@ class BatchSolver:
         self.cfg = cfg
         I = len(instances)
         blobs = [pack_instance(x) for x in instances]
+        for b, md in zip(blobs, self.modes):
+            require_time_packing(b, md)
         self.blobs_host = blobs
         offs = np.zeros(I, np.int64)
         offs[1:] = np.cumsum([len(b) for b in blobs[:-1]])
@@ -488,7 +488,7 @@ class BatchSolver:
         self.e_max = max(int(b[B_E]) for b in blobs)
         self.m_max = max(int(b[B_M]) for b in blobs)
         self.rmax_max = max(int(b[B_RMAX]) for b in blobs)
-        self.big_any = int(any(int(b[B_BIG]) for b in blobs))
+        self.no_big = int(not any(int(b[B_BIG]) for b in blobs))
         self.nbhd_max = max(1, max(neighborhood_size(int(b[B_N]), cfg.delta) for b in blobs))
         if self.nbhd_max >= KEY_LIMIT:
             raise UnsupportedInstance(f"neighbourhood of {self.nbhd_max} moves >= {KEY_LIMIT}")
@@ -595,7 +595,7 @@ class BatchSolver:
         a.cluster = (cfg.cluster if cfg.cluster is not None
                      else pick_cluster(n_group * cfg.workers))
         a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
-        a.big_any = self.big_any
+        a.no_big = self.no_big
         a.t0_ns = ptr(self.t0)
         return a
 
@@ -667,15 +667,22 @@ class BatchSolver:
             n_launches=self.launches, sgs_steps=int(ws[:, :, WK_FIELDS["sgs_steps"]].sum()))
 
     def run(self, stream=None) -> BatchResult:
-        """upload -> pool init -> search -> collect, timed with CUDA events."""
+        """upload -> pool init -> search -> collect.  Device time from CUDA
+        events around pool init + search; host wall time (perf_counter, the
+        reference's clock, cooperation.py:254/273) around upload + pool init
+        + search up to the stream synchronisation."""
         torch = _torch()
-        self.upload()
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         s = stream or torch.cuda.current_stream()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        tick = time.perf_counter()
+        self.upload()
         e0.record(s)
         self.pool_init(s)
         e1.record(s)
         self.search(stream=s)
         e2.record(s)
         e2.synchronize()
-        return self.collect(e0.elapsed_time(e2), e1.elapsed_time(e2))
+        wall = time.perf_counter() - tick
+        res = self.collect(e0.elapsed_time(e2), e1.elapsed_time(e2))
+        res.wall_s = wall
+        return res

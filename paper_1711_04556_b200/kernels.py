@@ -19,6 +19,7 @@ accepted for signature compatibility; the device keeps its own scratch.
 
 from __future__ import annotations
 
+import hashlib
 import os
 
 import numpy as np
@@ -45,13 +46,32 @@ BACKEND = _pick_backend()
 _inst_cache: dict = {}
 
 
+def _digest(*arrays) -> bytes:
+    """Content key of the operator's instance arrays: shapes, dtypes and
+    every byte (buffer addresses are not identities -- callers mutate arrays
+    in place and numpy reuses freed memory)."""
+    h = hashlib.blake2b(digest_size=20)
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(repr((a.shape, a.dtype.str)).encode())
+        h.update(a.tobytes())
+    return h.digest()
+
+
+def _remember(key: bytes, inst):
+    if len(_inst_cache) > 64:
+        _inst_cache.clear()
+    _inst_cache[key] = inst
+    return inst
+
+
 def _instance(durations, demands, capacities, pred_ptr, pred_dat):
-    """ProjectInstance whose predecessor lists are the given CSR (cached)."""
-    key = (durations.ctypes.data, demands.ctypes.data, capacities.ctypes.data,
-           pred_ptr.ctypes.data, pred_dat.ctypes.data, len(durations), len(pred_dat))
+    """ProjectInstance whose predecessor lists are the given CSR (cached by
+    the content of all five arrays)."""
+    key = _digest(durations, demands, capacities, pred_ptr, pred_dat)
     hit = _inst_cache.get(key)
-    if hit is not None and np.array_equal(hit[1], pred_dat) and np.array_equal(hit[2], durations):
-        return hit[0]
+    if hit is not None:
+        return hit
     n = len(durations)
     succ = [[] for _ in range(n)]
     for j in range(n):
@@ -60,24 +80,19 @@ def _instance(durations, demands, capacities, pred_ptr, pred_dat):
     inst = make_instance("kernel-args", np.asarray(durations).tolist(),
                          np.asarray(capacities).tolist(),
                          np.asarray(demands).reshape(n, -1).tolist(), succ)
-    if len(_inst_cache) > 64:
-        _inst_cache.clear()
-    _inst_cache[key] = (inst, np.array(pred_dat, copy=True), np.array(durations, copy=True))
-    return inst
+    return _remember(key, inst)
 
 
 def _adj_instance(adjacency):
     """Instance carrying only the precedence graph of a dense adjacency."""
     adjacency = np.asarray(adjacency, dtype=bool)
-    key = ("adj", adjacency.ctypes.data, adjacency.shape)
+    key = b"adj" + _digest(adjacency)
     hit = _inst_cache.get(key)
-    if hit is not None and np.array_equal(hit[1], adjacency):
-        return hit[0]
+    if hit is not None:
+        return hit
     n = adjacency.shape[0]
     succ = [list(np.nonzero(adjacency[i])[0]) for i in range(n)]
-    inst = make_instance("adjacency", [0] * n, [1], [[0]] * n, succ)
-    _inst_cache[key] = (inst, adjacency.copy())
-    return inst
+    return _remember(key, make_instance("adjacency", [0] * n, [1], [[0]] * n, succ))
 
 
 def evaluate_order(order, durations, demands, capacities, pred_ptr, pred_dat, mode, horizon,

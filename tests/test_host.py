@@ -168,8 +168,16 @@ def test_pack_instance_layout(ginst):
     roomy = ginst["roomy"]           # capacities 999 -> 16-bit lanes
     assert device.packing_for(roomy.capacities) == (16, 1)
     assert device.packing_for(np.array([10] * 5)) == (8, 2)
-    with pytest.raises(device.UnsupportedInstance):
-        device.packing_for(np.array([10] * 9))
+    # no TIME packing: the blob still builds (CAPACITY mode), TIME is refused
+    assert device.packing_for(np.array([10] * 9)) == (0, 0)
+    assert device.packing_for(np.array([200] * 5)) == (0, 0)
+    wide = make_instance("wide", [0, 2, 0], [10] * 9, [[0] * 9, [3] * 9, [0] * 9],
+                         [[1], [2], []])
+    blob = device.pack_instance(wide)
+    assert blob[device.B_W] == 0 and blob[device.B_LB] == 0
+    with pytest.raises(device.UnsupportedInstance, match="CAPACITY"):
+        device.require_time_packing(blob, device.MODE_TIME)
+    device.require_time_packing(blob, device.MODE_CAPACITY)
 
 
 def test_pack_rejects_overload():
@@ -183,7 +191,8 @@ def test_library_exports_every_declared_symbol():
     declares; no CUDA call is made."""
     from paper_1711_04556_b200 import _native
     header = (ROOT / "include" / "rcpsp_tabu_b200.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|const char \*)\s*\*?(rcpsp_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*\*?(rcpsp_\w+)\(", header,
+                              re.M))
     assert declared, "no declarations parsed"
     assert declared == set(_native.EXPORTED)
     if not _native.LIB_PATH.exists():
@@ -253,3 +262,69 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_operator_instance_cache_follows_content(ginst):
+    """The operator layer's instance cache is keyed by array content: mutating
+    the caller's demands / capacities in place (same buffer addresses) must
+    give a new instance, not the cached one (kernels.py cache)."""
+    from paper_1711_04556_b200 import kernels
+    inst = ginst["genr30s0"]
+    ka = inst.kernel_arrays
+    dur = np.array(ka.durations, np.int32)
+    dem = np.array(ka.demands, np.int32)
+    cap = np.array(ka.capacities, np.int32)
+    pp, pd = np.array(ka.pred_ptr, np.int32), np.array(ka.pred_dat, np.int32)
+    first = kernels._instance(dur, dem, cap, pp, pd)
+    assert first.demands.tolist() == inst.demands.tolist()
+    assert kernels._instance(dur, dem, cap, pp, pd) is first   # same content: cached
+    dem[:] = 0
+    cap += 5
+    second = kernels._instance(dur, dem, cap, pp, pd)
+    assert second is not first
+    assert int(second.demands.sum()) == 0
+    assert second.capacities.tolist() == cap.tolist()
+
+
+def test_tabu_state_mirror_semantics():
+    """TabuState: eviction, duplicate moves, snapshot/load, reference views."""
+    st = TabuState(12, size=3)
+    for mv in [(1, 2), (3, 5), (1, 2)]:
+        st.add(*mv)
+    assert st.is_tabu(1, 2) and st.is_tabu(3, 5) and len(st) == 3 and st.head == 0
+    st.add(4, 6)                       # evicts the first (1, 2); the copy keeps it tabu
+    assert st.is_tabu(1, 2) and st.counts[1, 2] == 1 and st.head == 1
+    st.add(7, 8)                       # evicts (3, 5)
+    assert not st.is_tabu(3, 5)
+    assert st.entries.tolist() == [[4, 6], [7, 8], [1, 2]]
+    ent, head = st.snapshot()
+    other = TabuState(12, 3)
+    other.load(ent, head)
+    assert other.entries.tolist() == st.entries.tolist() and other.head == st.head
+    assert (other.counts == st.counts).all()
+    assert other.packed.tolist() == [(4 << 16) | 6, (7 << 16) | 8, (1 << 16) | 2]
+    st.reset()
+    assert len(st) == 0 and not st.counts.any()
+    with pytest.raises(ValueError):
+        TabuState(5, 0)
+
+
+def test_moves_host_helpers(ginst):
+    """moves.py: validity, neighbourhood generation, swap feasibility (position
+    bounds) against brute force over the direct edges."""
+    from paper_1711_04556_b200 import apply_swap, is_swap_feasible
+    from conftest import random_topological_order
+    inst = ginst["genr30s0"]
+    rng = np.random.default_rng(3)
+    order = random_topological_order(inst, rng)
+    assert is_order_valid(inst, order)
+    nb = generate_reduced_neighborhood(order, 7)
+    want = [(u, v) for u in range(1, len(order) - 2)
+            for v in range(u + 1, min(u + 7, len(order) - 2) + 1)]
+    assert [tuple(x) for x in nb.tolist()] == want
+    for u, v in want[::5]:
+        sw = apply_swap(order, (u, v))
+        assert sw[u] == order[v] and sw[v] == order[u]
+        assert is_swap_feasible(order, (u, v), inst) == is_order_valid(inst, sw)
+    with pytest.raises(ValueError):
+        is_swap_feasible(order, (0, 3), inst)
