@@ -70,9 +70,12 @@ def parse():
                     help="evaluate every swap by a full SGS (no prefix reuse)")
     ap.add_argument("--no-steal", action="store_true",
                     help="fixed worker-to-instance mapping (no tail balancing)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0,
-                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="instances in the CPU sample (default synth.CPU_SAMPLE = 30): "
+                         "cpu_baseline and the reference arm time the same ones")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true",
+                    help="skip the j60p / act300 (TIME and CAPACITY) entries")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-quality", action="store_true",
                     help="skip the fixed-wall-clock CPM-deviation comparison")
@@ -153,70 +156,126 @@ def workload_name(cfg: str) -> str:
     return f"{cfg}-shape Gen-R batch (reference benchmark recipe)"
 
 
-SAMPLE_STRIDE = 157  # coprime with the batch sizes used: the sample spreads over the batch
-
-
-def sample_index(k: int, batch: int) -> int:
-    """Batch index of the k-th CPU-sample instance (spread over Gen-P's grid cells)."""
-    return (k * SAMPLE_STRIDE) % batch
-
-
-def cpu_sample(cfg: str, iters: int, target_s: float, threads: int, batch: int,
-               seed: int = 0) -> dict:
-    """Time the reference algorithm (C port, `threads` workers per instance,
-    instances one after another like `rcpsp-tabu bench`) on a bounded sample
-    of the workload: instances sample_index(0..) of the step's batch.  Returns
-    schedules/sec, the sample and the CPM deviation."""
+def host_cpu() -> dict:
+    """Host CPU model (lscpu 'Model name') and the cores this process may use."""
     import oracle
-    from paper_1711_04556_b200 import extract_features, decide_static, synth
-    evals = 0
-    wall = 0.0
-    devs = []
-    k = 0
-    while True:
-        inst = synth.benchmark_batch(cfg, 1, first_seed=sample_index(k, batch))[0]
-        mode = int(decide_static(extract_features(inst)))
-        r = oracle.orchestrate(inst, iters, threads, seed, mode)
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.split(":")[0].strip() == "Model name":
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    if model is None and Path("/proc/cpuinfo").exists():
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    return {"model": model, "cores": oracle.cpu_count(), "nproc": os.cpu_count()}
+
+
+def workload_config(cfg: str, insts, modes, params, iters: int) -> dict:
+    """The workload both arms run (identical dict in both JSON lines)."""
+    return {"workload": f"{workload_name(cfg)}, static-rule mode selection",
+            "instances": len(insts), "iters_per_instance": iters,
+            "pool_size": params.pool_size, "delta": params.delta, "tabu_size": params.tabu_size,
+            "modes": {"TIME": modes.count(1), "CAPACITY": modes.count(0)}}
+
+
+def solve_cpu(insts, modes, indices, iters: int, threads: int, seed: int = 0) -> dict:
+    """The reference algorithm (C port, `threads` workers per instance) on the
+    given batch indices, one instance after another like `rcpsp-tabu bench`;
+    schedules/sec = evaluations / wall summed over the instances
+    (cooperation.py:254-293, cli.py:236)."""
+    import oracle
+    evals, wall, devs = 0, 0.0, []
+    for i in indices:
+        r = oracle.orchestrate(insts[i], iters, threads, seed, modes[i])
         evals += r["evaluations"]
         wall += r["wall_time"]
         devs.append(100.0 * (r["best_cmax"] - r["critical_path"]) / r["critical_path"])
-        k += 1
-        if wall >= target_s or k >= 64:
-            break
-    return {"value": evals / wall, "evaluations": evals, "wall": wall, "instances": k,
-            "cpm_dev": float(np.mean(devs)), "iters": iters, "threads": threads}
+    return {"evaluations": evals, "wall": wall, "instances": len(indices),
+            "value": evals / wall if wall > 0 else 0.0,
+            "cpm_dev": float(np.mean(devs)) if devs else None, "iters": iters,
+            "threads": threads, "indices": list(indices)}
+
+
+def batch_and_modes(cfg: str, count: int, mode: str = "rule"):
+    from paper_1711_04556_b200 import decide_static, extract_features, synth
+    insts = synth.benchmark_batch(cfg, count)
+    if mode == "rule":
+        modes = [int(decide_static(extract_features(x))) for x in insts]
+    else:
+        modes = [1 if mode == "time" else 0] * len(insts)
+    return insts, modes
+
+
+def cpu_baseline(cfg: str, insts, modes, iters: int, count: int, w1: bool = True) -> dict:
+    """cpu_baseline object: the CPU sample on all host cores, plus a W = 1
+    number (one worker thread) on the sample's first two instances at a
+    fifth of the iterations."""
+    from paper_1711_04556_b200 import synth
+    hc = host_cpu()
+    idx = synth.sample_indices(cfg, count, len(insts))
+    cb = solve_cpu(insts, modes, idx, iters, hc["cores"])
+    out = {"value": cb["value"], "unit": "schedules/s", "cores": hc["cores"], "kind": "port",
+           "cpu_model": hc["model"], "nproc": hc["nproc"],
+           "sample": (f"{cb['instances']} {cfg} instances of the {len(insts)}-instance batch "
+                      f"(indices k*{synth.SAMPLE_STRIDE} mod {len(insts)}), I_total={iters}, "
+                      f"{hc['cores']} worker threads each, instances one after another, "
+                      f"{cb['wall']:.1f} s; cpm_dev {cb['cpm_dev']:.2f}%"),
+           "cpm_dev": cb["cpm_dev"], "wall_s": cb["wall"]}
+    if w1:
+        one = solve_cpu(insts, modes, idx[:2], max(50, iters // 5), 1)
+        out["w1"] = {"value": one["value"], "unit": "schedules/s", "cores": 1,
+                     "sample": f"first 2 sample instances, I_total={one['iters']}, 1 worker",
+                     "wall_s": one["wall"]}
+    return out, cb
 
 
 def run_reference(args, ws: int, rank: int) -> None:
+    """--impl reference: the reference algorithm (C port) on all host cores
+    over the SAME instance sample as the b200 arm's cpu_baseline, split over
+    the timed steps (step i solves sample instances [i*S/K, (i+1)*S/K), the
+    whole sample once over K steps; K > S cycles).  Rank 0 only."""
     if rank != 0:
         return
-    import oracle
-    cores = oracle.cpu_count()
-    iters = args.iters
-    per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(args.config, min(iters, 50), 0.5, cores, args.instances)
-    vals, evals, walls, devs = [], 0, 0.0, []
-    for _ in range(args.steps):
-        r = cpu_sample(args.config, iters, per_step, cores, args.instances)
-        vals.append(r["value"])
+    from paper_1711_04556_b200 import SearchParams, synth
+    insts, modes = batch_and_modes(args.config, args.instances, args.mode)
+    hc = host_cpu()
+    S = args.cpu_sample or synth.CPU_SAMPLE
+    idx = synth.sample_indices(args.config, S, len(insts))
+    K = max(1, args.steps)
+    for w in range(args.warmup):            # warm-up: short solves on the sample
+        solve_cpu(insts, modes, [idx[w % S]], min(args.iters, 50), hc["cores"])
+    evals, wall, devs, step_ms = 0, 0.0, [], []
+    for i in range(K):
+        part = idx[i * S // K:(i + 1) * S // K] if K <= S else [idx[i % S]]
+        r = solve_cpu(insts, modes, part, args.iters, hc["cores"])
         evals += r["evaluations"]
-        walls += r["wall"]
-        devs.append(r["cpm_dev"])
-    value = evals / walls
-    sample = (f"{r['instances']} {args.config} instances of the {args.instances}-instance batch "
-              f"(indices k*{SAMPLE_STRIDE} mod {args.instances}), I_total={iters}, "
-              f"{cores} worker threads per instance, instances solved one after another "
-              f"(~{per_step:.0f} s per step)")
+        wall += r["wall"]
+        step_ms.append(1e3 * r["wall"])
+        if r["cpm_dev"] is not None:
+            devs.append((r["cpm_dev"], r["instances"]))
+    value = evals / wall if wall > 0 else 0.0
+    p = SearchParams.defaults_for(insts[0].n_activities, total_iters=args.iters)
+    cpm = sum(d * k for d, k in devs) / max(1, sum(k for _, k in devs))
+    sample = (f"{S} {args.config} instances of the {len(insts)}-instance batch (indices "
+              f"k*{synth.SAMPLE_STRIDE} mod {len(insts)}, the b200 arm's cpu_baseline sample), "
+              f"split over {K} steps, I_total={args.iters}, {hc['cores']} worker threads per "
+              f"instance, instances one after another")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "schedules/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * walls / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{workload_name(args.config)}, reference C port on host",
-                   "iters_per_instance": iters, "cpm_dev": float(np.mean(devs))},
-        "cpu_baseline": {"value": value, "unit": "schedules/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "config": workload_config(args.config, insts, modes, p, args.iters),
+        "run": {"cpm_dev": cpm, "evaluations": evals, "wall_s": wall,
+                "executor": "reference algorithm, C port of the numba path (oracle/), host"},
+        "cpu_baseline": {"value": value, "unit": "schedules/s", "cores": hc["cores"],
+                         "kind": "port", "cpu_model": hc["model"], "sample": sample},
         "e2e": {"value": value, "unit": "schedules/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -235,8 +294,8 @@ def quality_leg(args, insts, modes, cb: dict) -> dict:
     import torch
     from paper_1711_04556_b200 import SearchParams
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
-    K = int(cb["instances"])
-    pick = [sample_index(k, len(insts)) for k in range(K)]  # the CPU sample's instances
+    pick = cb["indices"]                       # the CPU sample's instances
+    K = len(pick)
     qi, qm = [insts[i] for i in pick], [modes[i] for i in pick]
     # every CTA must be resident from the start (2 per SM): a wave that starts
     # after the clock stopped the search would never run
@@ -257,7 +316,82 @@ def quality_leg(args, insts, modes, cb: dict) -> dict:
                     "kind": "port", "workers_per_instance": cb.get("threads")},
             "gpu": {"cpm_dev": dev, "iters_per_instance": float(np.mean(res.iterations)),
                     "workers_per_instance": workers, "device_s": res.device_ms * 1e-3,
+                    "host_wall_s": res.wall_s,
                     "stop": "device clock (%globaltimer), 97 % of the budget"}}
+
+
+#: compact entries beside the headline (BASELINE.json configs[1] and [4]):
+#: (config, mode, workers per instance, I_total per instance)
+PER_CONFIG = (("j60p", "time", 8, 1000), ("j60p", "capacity", 8, 1000),
+              ("act300", "time", 2, 100), ("act300", "capacity", 2, 100))
+
+
+def per_config_entry(args, cfg: str, mode: str, workers: int, iters: int, smem_peak: float,
+                     cpu_count: int) -> dict:
+    """One compact measurement of another BASELINE config: the synth batch of
+    DEFAULT_BATCH instances, mode forced, 1 warm-up + 2 timed steps (CUDA
+    events around pool init + search, L2 flushed), its roofline fraction with
+    the same SMEM peak, and its own cpu_baseline on the config's CPU sample
+    (as many sample instances as fit ~4 s on all host cores, >= 2)."""
+    import torch
+    from paper_1711_04556_b200 import SearchParams, synth
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts, modes = batch_and_modes(cfg, synth.DEFAULT_BATCH[cfg], mode)
+    p = SearchParams.defaults_for(insts[0].n_activities, total_iters=iters, workers=workers,
+                                  seed=0)
+    scfg = SolveConfig(total_iters=iters, workers=workers, pool_size=p.pool_size,
+                       tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
+                       phi_max=p.phi_max, seed=0)
+    solver = BatchSolver(insts, modes, scfg)
+    solver.upload()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    ms, sms, evals, sevals, steps, devs = 0.0, 0.0, 0, 0, 0, []
+    for k in range(3):
+        solver.reset()
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        solver.pool_init(stream)
+        e1.record(stream)
+        solver.search(stream=stream)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        if k == 0:
+            continue
+        res = solver.collect()
+        ms += e0.elapsed_time(e2)
+        sms += e1.elapsed_time(e2)
+        evals += int(res.evaluations.sum())
+        sevals += int((res.evaluations - res.pool_evaluations).sum())
+        steps += res.sgs_steps
+        devs.append(float(np.mean(100.0 * (res.best_cmax - res.critical_path)
+                                  / res.critical_path)))
+    W = work_per_schedule(cfg)["time" if mode == "time" else "cap"]
+    achieved = sevals * W["bytes"] / (sms * 1e-3) / 1e9
+    # CPU sample: sample instances one by one until ~4 s
+    idx = synth.sample_indices(cfg, synth.CPU_SAMPLE, len(insts))
+    done, ev, wall = [], 0, 0.0
+    for i in idx:
+        r = solve_cpu(insts, modes, [i], iters, cpu_count)
+        ev += r["evaluations"]
+        wall += r["wall"]
+        done.append(r["cpm_dev"])
+        if wall >= 4.0 and len(done) >= 2:
+            break
+    return {"config": cfg, "mode": mode.upper(), "instances": len(insts),
+            "workers_per_instance": workers, "iters_per_instance": iters,
+            "value": evals / (ms * 1e-3), "unit": "schedules/s", "ms_per_step": ms / 2,
+            "cpm_dev": float(np.mean(devs)),
+            "roofline": {"achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                         "frac": achieved / smem_peak if smem_peak else None,
+                         "bytes_per_schedule": W["bytes"],
+                         "sgs_steps_per_schedule": steps / max(1, sevals)},
+            "cpu_baseline": {"value": ev / wall if wall else 0.0, "unit": "schedules/s",
+                             "cores": cpu_count, "kind": "port",
+                             "sample": f"{len(done)} sample instances, I_total={iters}, "
+                                       f"{wall:.1f} s", "cpm_dev": float(np.mean(done))}}
 
 
 def main() -> None:
@@ -280,15 +414,11 @@ def main() -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
             dist.init_process_group(backend)
-    from paper_1711_04556_b200 import SearchParams, decide_static, extract_features, synth
+    from paper_1711_04556_b200 import SearchParams, synth
     from paper_1711_04556_b200.device import (BatchSolver, SolveConfig, smem_bandwidth)
     from paper_1711_04556_b200.population import EliteExchange, run_epochs
 
-    insts = synth.benchmark_batch(args.config, args.instances)
-    if args.mode == "rule":
-        modes = [int(decide_static(extract_features(x))) for x in insts]
-    else:
-        modes = [1 if args.mode == "time" else 0] * len(insts)
+    insts, modes = batch_and_modes(args.config, args.instances, args.mode)
     p = SearchParams.defaults_for(insts[0].n_activities, total_iters=args.iters,
                                   workers=args.workers, seed=1000 * rank)
     cfg = SolveConfig(total_iters=p.total_iters, workers=p.workers, pool_size=p.pool_size,
@@ -419,27 +549,27 @@ def main() -> None:
         if rec:
             traffic = rec["dram_bytes_per_schedule"] * search_evals / (args.steps * epochs)
 
+    if ws > 1:
+        par = (f"{ws} independent search populations (one per GPU), elite exchange "
+               f"between {epochs} epochs by all_gather over {backend}")
+    else:
+        par = "1 search population on 1 GPU (no exchange)"
     line = {
         "metric": METRIC, "value": value, "unit": "schedules/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": f"{workload_name(args.config)}, static-rule mode selection",
-                   "instances": I,
-                   "workers_per_instance": args.workers, "iters_per_instance": args.iters,
-                   "pool_size": p.pool_size, "delta": p.delta, "tabu_size": p.tabu_size,
-                   "modes": {"TIME": modes.count(1), "CAPACITY": modes.count(0)},
-                   "epochs": epochs, "cpm_dev": float(np.mean(devs)),
-                   "evaluations_per_step": evals // args.steps,
-                   "iterations_per_step": iters_done // args.steps,
-                   "l2": "256 MiB buffer written between timed steps",
-                   "parallelism": f"{ws} independent populations" + (
-                       ", NCCL all_gather elite exchange" if ws > 1 else "")},
+        "config": workload_config(args.config, insts, modes, p, args.iters),
+        "run": {"workers_per_instance": args.workers, "epochs": epochs,
+                "cpm_dev": float(np.mean(devs)), "evaluations_per_step": evals // args.steps,
+                "iterations_per_step": iters_done // args.steps,
+                "l2": "256 MiB buffer written between timed steps", "parallelism": par},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "k_solve", "bytes_per_schedule": bytes_per_sched,
                      "bytes_basis": "reference full-SGS element touches x 4 B per evaluated "
-                                    "schedule (profiles/work_per_schedule.json)",
+                                    "schedule (profiles/work_per_schedule.json, pinned over "
+                                    "the CPU sample's instances)",
                      "sgs_steps_per_schedule": sgs_steps / max(1, search_evals),
                      "executed_step_fraction": sgs_steps / max(1, search_evals * n_act),
                      "peak_source": "measured in this run: rcpsp_smem_probe (LDS.128 stream)",
@@ -452,17 +582,15 @@ def main() -> None:
                 "d2h_bytes_per_step": d2h},
     }
     if ws == 1 and not args.no_cpu_baseline:
-        import oracle
-        cores = oracle.cpu_count()
-        cb = cpu_sample(args.config, args.iters, args.cpu_seconds, cores, args.instances)
-        line["cpu_baseline"] = {
-            "value": cb["value"], "unit": "schedules/s", "cores": cores, "kind": "port",
-            "sample": f"{cb['instances']} {args.config} instances of the batch "
-                      f"(indices k*{SAMPLE_STRIDE} mod {args.instances}), "
-                      f"I_total={cb['iters']}, {cores} worker threads each, "
-                      f"{cb['wall']:.1f} s; cpm_dev {cb['cpm_dev']:.2f}%"}
+        cb_line, cb = cpu_baseline(args.config, insts, modes, args.iters,
+                                   args.cpu_sample or synth.CPU_SAMPLE)
+        line["cpu_baseline"] = cb_line
         if not args.no_quality:
             line["quality"] = quality_leg(args, insts, modes, cb)
+    if ws == 1 and not args.no_per_config:
+        cores = host_cpu()["cores"]
+        line["per_config"] = [per_config_entry(args, c, m, w, it, peak, cores)
+                              for c, m, w, it in PER_CONFIG]
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

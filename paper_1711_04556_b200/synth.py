@@ -174,3 +174,22 @@ def benchmark_batch(config: str, count: int, first_seed: int = 0) -> list[Projec
     n_real, m = kw.pop("n_real"), kw.pop("m")
     return [random_instance(n_real, m, seed=s, **kw)
             for s in range(first_seed, first_seed + count)]
+
+
+#: instances per benchmark step (bench.py): the size of PSPLIB's j120 set
+#: (600) for the j120 configs, one instance per SM otherwise
+DEFAULT_BATCH = {"j30": 148, "j60": 148, "j120": 600, "act300": 148, "j30p": 148,
+                 "j60p": 148, "j120p": 600}
+#: the CPU sample: instances k * SAMPLE_STRIDE mod batch, k < CPU_SAMPLE -- the
+#: stride is coprime with every batch size, so the sample spreads over the
+#: batch (and over Gen-P's parameter-grid cells, 10 consecutive per cell)
+SAMPLE_STRIDE = 157
+CPU_SAMPLE = 30
+
+
+def sample_indices(config: str, count: int = CPU_SAMPLE, batch: int | None = None) -> list[int]:
+    """Batch indices of the CPU-sample instances of a benchmark config (bench.py's
+    cpu_baseline, its reference arm and quality leg, and the pinned W of
+    profiles/work_per_schedule.json all use this sample)."""
+    batch = DEFAULT_BATCH[config] if batch is None else batch
+    return [(k * SAMPLE_STRIDE) % batch for k in range(count)]

@@ -252,7 +252,7 @@ def test_bench_reference_arm_contract():
     import sys
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
                           "--config", "j30p", "--instances", "40", "--steps", "1",
-                          "--warmup", "0", "--cpu-seconds", "1", "--iters", "50"],
+                          "--warmup", "0", "--cpu-sample", "2", "--iters", "50"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
