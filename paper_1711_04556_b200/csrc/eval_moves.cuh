@@ -303,13 +303,21 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req,
   }
 }
 
-// CAP, one warp per schedule (sgs.cuh: cap_step_warp), reusing the current
-// order's schedule prefix like eval_moves_time32_inc.  Alg. 4 is not
-// invertible and its state depends on the update order (not only on the set
-// of starts), so there is no undo and no convergence exit: each move copies
-// the prefix state (c_pre, es_pre) and schedules positions u..n-1.  With
-// reuse == false the prefix stays empty (full SGS of every swapped order).
-//   per-warp scratch: c [m*rs] | cb [m*rs] | es [n] | c_pre [m*rs] | es_pre [n]
+// CAP, one warp per schedule, reusing the current order's schedule prefix
+// like eval_moves_time32_inc.  Alg. 4 runs in closed form with the whole warp
+// (sgs.cuh: cap_update_warp).  Its state depends on the update order, not
+// only on the set of starts, so there is no undo and no convergence exit:
+// each move copies the prefix state c_pre and schedules positions u..n-1.
+// Precedence is pulled as in the TIME evaluator: es = max over the
+// predecessors' finish times fin[] (the prefix activities hold the current
+// schedule's, the suffix overwrites its own before a successor reads them),
+// so no per-move es copy.  With reuse == false the prefix stays empty (full
+// SGS of every swapped order).  The zero-duration sink is not scheduled (its
+// start, max(es, Eq. 7), is bounded by the finish times already in the
+// makespan).
+//   per-warp scratch: c [m*rs] | c_pre [m*rs] | fin [n]
+//   o_info: pull records (info_r); o_pull: padded predecessor lists (pdat)
+template <bool BIG>
 __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_dem, int o_cap,
                                                  int o_base, int o_bst, int o_ctr, int o_evs,
                                                  int n, int m, int rs,
@@ -319,14 +327,15 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mr = m * rs;
   const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
-  const uint32_t a_c = a_scr, a_cb = a_c + 4 * mr, a_es = a_cb + 4 * mr, a_cp = a_es + 4 * n,
-                 a_esp = a_cp + 4 * mr;
-  const uint32_t a_info = sa(dsm + o_info), a_push = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
+  const uint32_t a_c = a_scr, a_cp = a_c + 4 * mr, a_fin = a_cp + 4 * mr;
+  const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr);
+  const uint32_t a_pdat_l = opaque(a_pdat + 4 * lane);
   const int capk = lane < m ? dsm[o_cap + lane] : 0;
   for (int j = lane; j < mr; j += 32) sts32(a_cp + 4 * j, 0);
-  for (int a = lane; a < n; a += 32) sts32(a_esp + 4 * a, 0);
   __syncwarp();
+  const int pend = lds128(a_info + 16 * static_cast<int>(lds32(a_base + 4 * (n - 1)))).x == 0
+                       ? n - 1 : n;
   int up = 0, cm_pre = 0, steps = 0;
   for (;;) {
     int idx = 0;
@@ -339,36 +348,41 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
     // ---- extend the prefix state to positions < u0 with the known starts
     for (; up < u0; ++up) {
       const int act = static_cast<int>(lds32(a_base + 4 * up));
-      const int4 rec = lds128(a_info + 16 * act);
+      const int dur = lds128(a_info + 16 * act).x;
       const int st = static_cast<int>(lds32(a_bst + 4 * act));
-      if (rec.x > 0) {
+      if (dur > 0) {
         const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
-        cap_commit_all(a_cp, a_cb, rs, m, capk, req, st, rec.x);
+        cap_update_all(a_cp, rs, m, capk, req, st, dur);
       }
-      const int fin = st + rec.x;
-      cm_pre = max(cm_pre, fin);
-      const int e0 = rec.z & 0xffff, ecnt = rec.z >> 16;
-      for (int e = lane; e < ecnt; e += 32) {
-        const uint32_t adr = a_esp + 4 * lds32(a_push + 4 * (e0 + e));
-        if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-      }
+      cm_pre = max(cm_pre, st + dur);
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(st + dur));
       __syncwarp();
     }
     for (int j = lane; j < mr; j += 32) sts32(a_c + 4 * j, lds32(a_cp + 4 * j));
-    for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, lds32(a_esp + 4 * a));
     __syncwarp();
     // ---- positions u0.. of the swapped order
     int cm = cm_pre;
-    for (int p = u0; p < n; ++p) {
+    for (int p = u0; p < pend; ++p) {
       const int q = p == u ? v : (p == v ? u : p);
       const int act = static_cast<int>(lds32(a_base + 4 * q));
       const int4 rec = lds128(a_info + 16 * act);
-      const int esv = static_cast<int>(lds32(a_es + 4 * act));
-      cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_cb, a_push, rec.z & 0xffff,
-                    rec.z >> 16, a_es, cm);
+      const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
+      int f = static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat_l + 4 * p0)));
+      f = lane < pc ? f : 0;
+      if (BIG && pc > 32)
+        for (int e = lane + 32; e < pc; e += 32)
+          f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
+      const int esv = __reduce_max_sync(FULL_MASK, f);
+      int req;
+      const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req);
+      if (rec.x > 0) cap_update_all(a_c, rs, m, capk, req, start, rec.x);
+      const int fin = start + rec.x;
+      cm = max(cm, fin);
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
+      __syncwarp();
     }
     if (lane == 0) cmax_out[idx] = cm;
-    steps += n - u0;
+    steps += pend - u0;
   }
   if (lane == 0) {
     if (ctr_cl)
@@ -406,7 +420,7 @@ __device__ __noinline__ void eval_moves_cap(const SInst& I, int o_base, int o_ev
 // swapped order; positions u_min..u-1 are the current order's, booked at their
 // known starts.
 //   per-warp scratch: L lanes x (c [m*R] | cb [R] | es [n]) interleaved by lane
-//                     | c_pre [m*rs] | cb_w [rs] | es_pre [n]   (cap_prefix_words)
+//                     | c_pre [m*rs] | es_pre [n]   (cap_prefix_words)
 __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_base, int o_bst,
                                                        int o_ctr, int o_evs,
                                                        const uint32_t* __restrict__ moves,
@@ -419,9 +433,8 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
   const int* bst = dsm + o_bst;
   int* st = dsm + o_evs + warp * warp_words;
   int* cpre = st + L * cap_thread_words(n, m, R);
-  int* esp = cpre + (m + 1) * rs;
-  const uint32_t a_cpre = sa(cpre), a_cbw = sa(cpre + m * rs), a_dem = sa(I.dem),
-                 a_ctr = sa(dsm + o_ctr);
+  int* esp = cpre + m * rs;
+  const uint32_t a_cpre = sa(cpre), a_dem = sa(I.dem), a_ctr = sa(dsm + o_ctr);
   const int capk = lane < m ? I.cap[lane] : 0;
   int* c = st + lane;                     // c[(k*R + i)*L]
   int* cb = st + (m * R) * L + lane;      // cb[i*L]
@@ -450,7 +463,7 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
       const int dur = I.dur[act], s0 = bst[act];
       if (dur > 0) {
         const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
-        cap_commit_seq(a_cpre, a_cbw, rs, m, capk, req, s0, dur);
+        cap_update_all(a_cpre, rs, m, capk, req, s0, dur);
       }
       const int fin = s0 + dur;
       cm_pre = max(cm_pre, fin);
@@ -529,6 +542,21 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
                                     base_cmax, c.err, ctr_cl);
 }
 
+// the prefix-reusing CAPACITY warp evaluator on this CTA's copy of the current order
+__device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
+                                                             bool reuse, uint32_t ctr_cl) {
+  if (c.I.big)
+    eval_moves_cap_warp<true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
+                              soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
+                              c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
+                              n_feas, c.warp_words, reuse, ctr_cl);
+  else
+    eval_moves_cap_warp<false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
+                               soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
+                               c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
+                               n_feas, c.warp_words, reuse, ctr_cl);
+}
+
 // Cluster follower (rank > 0): evaluates moves of the leader's neighbourhood
 // phases until the leader is done.  Per phase: B1 (leader published the
 // phase), copy the current order and its starts from the leader's shared
@@ -561,10 +589,7 @@ __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, 
     if constexpr (MODE == MODE_TIME) {
       eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, ctr);
     } else if constexpr (G == 32) {
-      eval_moves_cap_warp(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.dem), soff(c.I.cap),
-                          soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.n,
-                          c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
-                          c.warp_words, true, ctr);
+      eval_moves_cap_warp_dispatch(c, n_feas, true, ctr);
     } else {
       eval_moves_cap_thread_inc(c.I, soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
                                 soff(c.evs), c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
@@ -629,10 +654,7 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
     }
     __syncthreads();
     cluster_phase_begin(c, n_feas);
-    eval_moves_cap_warp(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.dem), soff(c.I.cap),
-                        soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs), c.I.n,
-                        c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
-                        c.warp_words, c.inc, cluster_counter(c));
+    eval_moves_cap_warp_dispatch(c, n_feas, c.inc, cluster_counter(c));
     cluster_phase_end(c);
   } else {
     // prefix reuse pays from j60 on; on j30-size projects the per-batch state

@@ -302,15 +302,19 @@ __global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, R
   const int lane = threadIdx.x & 31;
   const int m = I.m, R = I.rmax, H = I.H, dur = I.dur[act];
   const int* dem = I.dem + act * m;
-  if (op == OP_CAP_ES || op == OP_CAP_UPDATE) {
-    if (lane == 0) {
-      if (op == OP_CAP_ES) {
-        out[0] = cap_es(state, 1, dem, I.cap, m, R);
-      } else {
-        cap_commit(state, smem + used, 1, dem, I.cap, m, R, arg, dur);
-        out[0] = 0;
-      }
-    }
+  if (op == OP_CAP_ES) {
+    if (lane == 0) out[0] = cap_es(state, 1, dem, I.cap, m, R);
+    return;
+  }
+  if (op == OP_CAP_UPDATE) {  // the SGS's warp-wide closed form of Alg. 4
+    int* st = smem + used;
+    for (int j = lane; j < m * R; j += 32) st[j] = state[j];
+    __syncwarp();
+    const int capk = lane < m ? I.cap[lane] : 0, req = lane < m ? dem[lane] : 0;
+    if (dur > 0) cap_update_all(sa(st), R, m, capk, req, arg, dur);
+    __syncwarp();
+    for (int j = lane; j < m * R; j += 32) state[j] = st[j];
+    if (lane == 0) out[0] = 0;
     return;
   }
   // TIME: pack [m][H+1] into lane words
@@ -1217,7 +1221,7 @@ int rcpsp_state_op(const int32_t* blob, const RcpspShape* shape, int op, int32_t
   if (op >= OP_TIME_ES && h.W == 0) return fail("instance has no TIME packing (CAPACITY only)");
   if (act < 0 || act >= h.n) return fail("activity out of range");
   const size_t words = ((inst_smem_words(h.n, h.m, h.e, h.W) + 3) & ~3) +
-                       static_cast<size_t>(std::max((h.H + 1) * h.W, h.rmax)) + 4;
+                       static_cast<size_t>(std::max((h.H + 1) * h.W, h.m * h.rmax)) + 4;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (h.W == 2) {
     if (set_smem(k_state_op<2>, words * 4)) return -1;

@@ -150,7 +150,7 @@ struct SmemPlan {
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes, int big = 1) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
-  if (G == 32) return cap_warp_words(n, m, rmax) + m * cap_row_stride(rmax) + n;
+  if (G == 32) return 2 * m * cap_row_stride(rmax) + n;  // c | c_pre | fin
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));
 }

@@ -584,207 +584,151 @@ __host__ __device__ __forceinline__ int cap_thread_words(int n, int m, int rmax)
 }
 
 // ---------------------------------------------------------------------------
-// Warp-cooperative capacity-indexed SGS (group 32): one warp per schedule,
-// lane k < m owns resource k -- its row of the state c_k and of the copy
-// buffer -- so Eq. 7's max over resources is one REDUX and the m Alg. 4
-// updates run side by side.  Rows are `rs` words apart (rmax rounded up to
-// odd: the m rows fall in distinct banks).
-//   scratch: c [m*rs] | cb [m*rs] | es [n]
+// Warp-cooperative capacity-indexed SGS (group 32): one warp per schedule.
+// Lane k < m holds resource k's capacity and demand, so Eq. 7's max over the
+// resources is one REDUX; Alg. 4 then runs per demanded resource with the
+// whole warp in closed form (cap_update_warp).  Rows are `rs` words apart
+// (rmax rounded up to odd: the m rows fall in distinct banks).
+//   scratch: c [m*rs] | es [n]
 
 __host__ __device__ __forceinline__ int cap_row_stride(int rmax) { return rmax | 1; }
 
 __host__ __device__ __forceinline__ int cap_warp_words(int n, int m, int rmax) {
-  return 2 * m * cap_row_stride(rmax) + n;  // c rows | copy-buffer rows | es
+  return m * cap_row_stride(rmax) + n;  // c rows | es (or fin)
 }
-// the thread-per-schedule evaluator's shared prefix: c rows | one copy-buffer
-// row | es (its updates run one resource after another, cap_commit_seq)
+// the thread-per-schedule evaluator's shared prefix: c rows | es
 __host__ __device__ __forceinline__ int cap_prefix_words(int n, int m, int rmax) {
-  return (m + 1) * cap_row_stride(rmax) + n;
+  return m * cap_row_stride(rmax) + n;
 }
 
-// Alg. 4 (kernels.py:81-110) on one resource row from entry i0 on, one
-// lane, quirks preserved.  Entries before i0 are the leading run with
-// c >= start + dur, which the reference's loop skips one by one.
-// (copy_idx0, effort0): resume after entries already processed (effort0 < 0:
-// the full effort req * dur, nothing processed yet)
-__device__ __forceinline__ void cap_commit_row(uint32_t a_c, uint32_t a_cb, int capk, int req,
-                                               int start, int dur, int i0 = 0,
-                                               int copy_idx0 = 0, int effort0 = -1) {
-  int effort = effort0 < 0 ? req * dur : effort0;
-  if (effort <= 0) return;
-  int copy_idx = copy_idx0, new_time = start + dur;
-  for (int i = i0; effort > 0 && i < capk; ++i) {
-    const int cv = static_cast<int>(lds32(a_c + 4 * i));
-    if (cv < new_time) {
-      if (copy_idx >= req) new_time = static_cast<int>(lds32(a_cb + 4 * (copy_idx - req)));
-      const int fl = cv < start ? start : cv;
-      const int diff = new_time - fl;
-      if (effort - diff > 0) {
-        effort -= diff;
-        sts32(a_cb + 4 * copy_idx, static_cast<uint32_t>(cv));
-        ++copy_idx;
-        sts32(a_c + 4 * i, static_cast<uint32_t>(new_time));
-      } else {
-        sts32(a_c + 4 * i, static_cast<uint32_t>(fl + effort));
-        effort = 0;
-      }
-    }
-  }
-}
-
-// Alg. 4 on one resource row, whole warp.  The leading run of entries with
-// c >= start + dur is found with ballots (the row is descending).  If the
-// first entry below start + dur is already free at `start`, so are the next
-// req - 1 (descending row, and Eq. 7 guarantees req entries <= start), and
-// the reference's loop sets exactly those req entries to start + dur -- done
-// by req lanes at once (~90-95 % of updates on the Gen-R configs).  Else
-// lane 0 runs the loop from i0.
-__device__ __forceinline__ void cap_commit_warp(uint32_t a_c, uint32_t a_cb, int capk, int req,
-                                                int start, int dur) {
-  if (req * dur <= 0) return;
+// Alg. 4 (kernels.py:81-110) on one resource row c[0..capk) (descending),
+// whole warp, in closed form -- the same result as the reference's loop for
+// every descending row with c[capk - r] <= s (Eq. 7), its quirks included
+// (exhaustively fuzzed against the loop: tests/test_gpu_state.py through
+// rcpsp_state_op, and the SGS parity tests).  With T = s + d and i0 the first
+// entry below T (the leading entries >= T are skipped):
+//  * c[i0] <= s: every entry from i0 on is free at s; the loop spends the
+//    effort r*d on exactly the r entries i0..i0+r-1, which become T;
+//  * else entries i0..i0+r-1 become T with a surplus E = sum (max(c,s) - s)
+//    > 0, and the loop then moves the row right by r (entry i takes the old
+//    c[i-r]; a run of equal entries it skips keeps the same value), spending
+//    c[i-r] - max(c[i], s) per entry while the surplus lasts.  With
+//    g(i) = s - max(c_i, s) for i < i0 + r, c_{i-r} - max(c_i, s) after, and
+//    S(i) = sum_{j=i0..i} g(j): it stops at the first t >= i0 + r with
+//    S(t) >= 0, setting c[t] = max(c_t, s) - S(t-1); the entries after t keep
+//    their values (no stop: the shift runs to the end of the row).
+// One warp-wide inclusive scan per 32 entries finds t; the reference's loop
+// walks the row entry by entry on one thread.
+__device__ __forceinline__ void cap_update_warp(uint32_t a_row, int capk, int r, int s, int d) {
   const int lane = threadIdx.x & 31;
-  const int T = start + dur;
-  int i0 = capk;
+  const int T = s + d;
+  int i0 = capk, c0 = 0;
   for (int b = 0; b < capk; b += 32) {
     const int i = b + lane;
-    const unsigned msk =
-        __ballot_sync(FULL_MASK, i < capk && static_cast<int>(lds32(a_c + 4 * i)) < T);
+    const int v = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+    const unsigned msk = __ballot_sync(FULL_MASK, i < capk && v < T);
     if (msk) {
-      i0 = b + __ffs(msk) - 1;
+      const int l = __ffs(msk) - 1;
+      i0 = b + l;
+      c0 = __shfl_sync(FULL_MASK, v, l);
       break;
     }
   }
-  if (i0 < capk) {
-    const int c0 = static_cast<int>(lds32(a_c + 4 * i0));
-    if (c0 <= start && i0 + req <= capk) {
-      for (int j = lane; j < req; j += 32) sts32(a_c + 4 * (i0 + j), static_cast<uint32_t>(T));
-    } else if (lane == 0) {
-      cap_commit_row(a_c, a_cb, capk, req, start, dur, i0);
-    }
-  }
+  if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
   __syncwarp();
-}
-
-// The m resource updates of one activity, one after another, whole warp.
-// req: lane k < m holds resource k's demand.
-// Alg. 4 for up to 4 resources at once: lanes 8k..8k+7 own resource k (its
-// state row and copy-buffer row).  The leading run of entries >= start + dur
-// is found by strided probing (8 probes per round narrow the range 8x; the
-// row is descending, so the probe verdicts are monotone), then the same fast
-// path / reference loop as cap_commit_warp.
-__device__ __forceinline__ void cap_commit_groups(uint32_t a_c, uint32_t a_cb, int rs, int m,
-                                                  int capk_k, int req_k, int start, int dur) {
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 3, j = lane & 7;
-  const int capk = __shfl_sync(FULL_MASK, capk_k, g);
-  const int req = __shfl_sync(FULL_MASK, req_k, g);
-  const bool act = g < m && req > 0;
-  const uint32_t row = a_c + 4 * g * rs, cbrow = a_cb + 4 * g * rs;
-  const int T = start + dur;
-  int lo = 0, hi = act ? capk : 0;  // first entry < T lies in [lo, hi), or there is none
-  while (__any_sync(FULL_MASK, hi - lo > 8)) {
-    const int span = hi - lo;
-    const bool nar = span > 8;
-    const int stride = (span + 7) >> 3;
-    const int idx = lo + j * stride;
-    const bool pr = nar && idx < hi && static_cast<int>(lds32(row + 4 * idx)) < T;
-    const uint32_t b = (__ballot_sync(FULL_MASK, pr) >> (8 * g)) & 0xffu;
-    if (nar) {
-      if (b) {
-        const int f = __ffs(b) - 1;  // first probe below T: the entry lies in (probe f-1, probe f]
-        hi = lo + f * stride + 1;
-        lo = f > 0 ? lo + (f - 1) * stride + 1 : lo;
-      } else {  // every probe inside the range is at or above T: past the last one
-        lo += min(7, (span - 1) / stride) * stride + 1;
-      }
-    }
-  }
-  const bool pr = j < hi - lo && static_cast<int>(lds32(row + 4 * (lo + j))) < T;
-  const uint32_t b = (__ballot_sync(FULL_MASK, pr) >> (8 * g)) & 0xffu;
-  const int i0 = b ? lo + __ffs(b) - 1 : capk;
-  const bool has = act && i0 < capk;
-  const int c0 = has ? static_cast<int>(lds32(row + 4 * i0)) : 0;
-  const bool fast = has && c0 <= start && i0 + req <= capk;
-  // c0 > start: the reference's loop processes exactly the req entries from i0
-  // with new_time = start + dur before the effort can run out (the effort left
-  // after entry k is (req-k-1)*dur + sum (max(c, start) - start) > 0), so those
-  // steps run side by side; the loop resumes after them with copy_idx = req
-  // and the effort still left
-  const bool ph1 = has && !fast && i0 + req <= capk;
-  int part = 0;
-  if (fast) {
-    for (int t = j; t < req; t += 8) sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
-  } else if (ph1) {
-    for (int t = j; t < req; t += 8) {
-      const int cv = static_cast<int>(lds32(row + 4 * (i0 + t)));
-      sts32(cbrow + 4 * t, static_cast<uint32_t>(cv));
-      sts32(row + 4 * (i0 + t), static_cast<uint32_t>(T));
-      part += max(cv, start) - start;
-    }
-  }
-  part += __shfl_xor_sync(FULL_MASK, part, 1);  // group sums (all lanes take part)
-  part += __shfl_xor_sync(FULL_MASK, part, 2);
-  part += __shfl_xor_sync(FULL_MASK, part, 4);
-  __syncwarp();
-  if (j == 0) {
-    if (ph1)
-      cap_commit_row(row, cbrow, capk, req, start, dur, i0 + req, req, part);
-    else if (has && !fast)
-      cap_commit_row(row, cbrow, capk, req, start, dur, i0);
-  }
-  __syncwarp();
-}
-
-// The m resource updates of one activity: side by side for m <= 4
-// (cap_commit_groups), else one after another with the whole warp.
-//   a_cb: m copy-buffer rows, rs words apart
-__device__ __forceinline__ void cap_commit_all(uint32_t a_c, uint32_t a_cb, int rs, int m,
-                                               int capk, int req, int start, int dur) {
-  if (m <= 4) {
-    cap_commit_groups(a_c, a_cb, rs, m, capk, req, start, dur);
+  if (c0 <= s) {
+    for (int j = lane; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
+    __syncwarp();
     return;
   }
-  for (int k = 0; k < m; ++k) {
-    const int rk = __shfl_sync(FULL_MASK, req, k);
-    const int ck = __shfl_sync(FULL_MASK, capk, k);
-    cap_commit_warp(a_c + 4 * k * rs, a_cb, ck, rk, start, dur);
+  int carry = 0, t = capk, newt = 0, b = i0, oir = 0;
+  for (;; b += 32) {
+    const int i = b + lane;
+    const bool in = i < capk, sh = i >= i0 + r;
+    const int oi = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+    oir = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
+    const int f = max(oi, s);
+    const int g = in ? (sh ? oir - f : s - f) : 0;
+    int S = g;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, S, o);
+      if (lane >= o) S += y;
+    }
+    S += carry;
+    const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
+    if (term) {
+      const int l = __ffs(term) - 1;
+      t = b + l;
+      newt = __shfl_sync(FULL_MASK, f - (S - g), l);
+      break;
+    }
+    if (b + 32 >= capk) break;
+    carry = __shfl_sync(FULL_MASK, S, 31);
   }
+  const int end = t < capk ? t : capk;  // [i0, end): T / shifted; t: newt
+  __syncwarp();
+  if (b == i0) {  // one chunk: every old value is in registers
+    const int i = i0 + lane;
+    if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : oir));
+    if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+  } else {
+    // backward over the chunks: a chunk reads c[i - r] (lower entries) before
+    // its lanes write, and no lower chunk has been written yet
+    for (int bb = b; bb >= i0; bb -= 32) {
+      const int i = bb + lane;
+      const int v = (i < end && i >= i0 + r) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : T;
+      __syncwarp();
+      if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(v));
+      if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+      __syncwarp();
+    }
+  }
+  __syncwarp();
 }
 
-// The m resource updates one after another with the whole warp, sharing one
-// copy-buffer row (a_cb: rs words)
-__device__ __forceinline__ void cap_commit_seq(uint32_t a_c, uint32_t a_cb, int rs, int m,
-                                               int capk, int req, int start, int dur) {
-  for (int k = 0; k < m; ++k) {
-    const int rk = __shfl_sync(FULL_MASK, req, k);
-    const int ck = __shfl_sync(FULL_MASK, capk, k);
-    cap_commit_warp(a_c + 4 * k * rs, a_cb, ck, rk, start, dur);
-  }
-}
-
-// One activity: start = max(es_prec, Eq. 7) (Eq. 7 also for zero durations,
-// as kernels.py:182-186), Alg. 4 per resource, push the finish time.
-//   capk: lane k < m holds resource k's capacity (lanes >= m: 0)
-//   a_c: the state rows (row k at a_c + 4*k*rs); a_cb: copy buffer [rmax]
-template <bool REC = false>
-__device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t a_dem, int m,
-                                             int capk, int rs, uint32_t a_c, uint32_t a_cb,
-                                             uint32_t a_push, int e0, int ecnt, uint32_t a_es,
-                                             int& cmax) {
+// Alg. 4 for every resource the activity demands (lane k < m: capacity and
+// demand of resource k), one after another with the whole warp.
+__device__ __forceinline__ void cap_update_all(uint32_t a_c, int rs, int m, int capk, int req,
+                                               int start, int dur) {
   const int lane = threadIdx.x & 31;
-  int req = 0, t = 0;
+  unsigned used = __ballot_sync(FULL_MASK, lane < m && req > 0);
+  while (used) {
+    const int k = __ffs(used) - 1;
+    used &= used - 1;
+    cap_update_warp(a_c + 4 * k * rs, __shfl_sync(FULL_MASK, capk, k),
+                    __shfl_sync(FULL_MASK, req, k), start, dur);
+  }
+}
+
+// Eq. 7 start (kernels.py:68-78, also for zero durations, as kernels.py:
+// 182-186) of an activity whose precedence bound is esv; req: lane k < m gets
+// resource k's demand.
+__device__ __forceinline__ int cap_start_warp(int act, int esv, uint32_t a_dem, int m, int capk,
+                                              int rs, uint32_t a_c, int& req) {
+  const int lane = threadIdx.x & 31;
+  int t = 0;
+  req = 0;
   if (lane < m) {
     req = static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
     if (req > 0) t = static_cast<int>(lds32(a_c + 4 * (lane * rs + capk - req)));
   }
-  const int start = max(esv, __reduce_max_sync(FULL_MASK, t));
-  if (dur > 0) cap_commit_all(a_c, a_cb, rs, m, capk, req, start, dur);
+  return max(esv, __reduce_max_sync(FULL_MASK, t));
+}
+
+// One activity, push form: start = max(es_prec, Eq. 7), Alg. 4 per resource,
+// the finish time pushed to the successors' es.
+//   capk: lane k < m holds resource k's capacity (lanes >= m: 0)
+__device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t a_dem, int m,
+                                             int capk, int rs, uint32_t a_c, uint32_t a_push,
+                                             int e0, int ecnt, uint32_t a_es, int& cmax) {
+  const int lane = threadIdx.x & 31;
+  int req;
+  const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req);
+  if (dur > 0) cap_update_all(a_c, rs, m, capk, req, start, dur);
   const int fin = start + dur;
   cmax = max(cmax, fin);
-  for (int e = lane; e < ecnt; e += 32) {
-    const uint32_t adr = a_es + 4 * lds32(a_push + 4 * (e0 + e));
-    if (static_cast<int>(lds32(adr)) < fin) sts32(adr, static_cast<uint32_t>(fin));
-  }
+  for (int e = lane; e < ecnt; e += 32) red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
   __syncwarp();
   return start;
 }
@@ -795,7 +739,7 @@ __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, ui
                                             const int* cap, int n, int m, int rs, uint32_t a_scr,
                                             uint32_t a_ord, int* __restrict__ starts_out) {
   const int lane = threadIdx.x & 31;
-  const uint32_t a_c = a_scr, a_cb = a_scr + 4 * m * rs, a_es = a_cb + 4 * m * rs;
+  const uint32_t a_c = a_scr, a_es = a_scr + 4 * m * rs;
   for (int j = lane; j < m * rs; j += 32) sts32(a_c + 4 * j, 0);
   for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
@@ -805,7 +749,7 @@ __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, ui
     const int act = static_cast<int>(lds32(a_ord + 4 * pos));
     const int4 rec = lds128(a_info + 16 * act);
     const int esv = static_cast<int>(lds32(a_es + 4 * act));
-    const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_cb, a_push,
+    const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_push,
                                 rec.z & 0xffff, rec.z >> 16, a_es, cmax);
     if (starts_out && lane == 0) starts_out[act] = s;
   }

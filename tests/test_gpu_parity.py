@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import chain_instance, random_topological_order
+from conftest import chain_instance, random_topological_order, random_topological_orders
 
 pytestmark = pytest.mark.gpu
 
@@ -48,27 +48,53 @@ def test_worked_example(ginst):
         assert evaluate(initial_order(roomy, False), roomy, mode).cmax == critical_path_length(roomy)
 
 
-@pytest.mark.parametrize("cfg,count", [("j30", 4000), ("j60", 3000), ("j120", 3000),
-                                       ("act300", 600)])
-def test_eval_fuzz_vs_oracle(cfg, count):
-    """>= 10^4 random precedence-feasible orders per config, both modes, every
-    group size, starts included; plus reversed-project evaluation."""
-    insts = synth.benchmark_batch(cfg, 2, first_seed=11)
-    rng = np.random.default_rng(5)
+FUZZ_CONFIGS = ("j30", "j60", "j120", "act300", "j30p", "j60p", "j120p")
+
+
+def _oracle_parallel(inst, orders, mode, reverse=False, chunks=16):
+    """oracle.evaluate_batch over row chunks in threads (ctypes drops the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    parts = np.array_split(orders, min(chunks, max(1, len(orders))))
+    with ThreadPoolExecutor(max_workers=chunks) as ex:
+        res = list(ex.map(lambda o: oracle.evaluate_batch(inst, o, mode, reverse=reverse), parts))
+    return np.concatenate([c for c, _ in res]), np.concatenate([s for _, s in res])
+
+
+def _fuzz(cfg, per_inst, n_inst, groups_time, groups_cap, seed):
+    insts = synth.benchmark_batch(cfg, n_inst, first_seed=11)
+    rng = np.random.default_rng(seed)
     for inst in insts:
-        orders = np.stack([random_topological_order(inst, rng) for _ in range(count // 2)])
+        orders = random_topological_orders(inst, rng, per_inst)
+        orders[: min(50, per_inst)] = np.stack(
+            [random_topological_order(inst, rng) for _ in range(min(50, per_inst))])
         for mode in (0, 1):
-            want_c, want_s = oracle.evaluate_batch(inst, orders, mode)
-            for group in GROUPS if mode == 1 else CAP_GROUPS:
+            want_c, want_s = _oracle_parallel(inst, orders, mode)
+            for group in groups_time if mode == 1 else groups_cap:
                 got_c, got_s = device.eval_batch(inst, orders, mode, group=group)
                 assert np.array_equal(got_c, want_c), (cfg, mode, group)
                 assert np.array_equal(got_s, want_s), (cfg, mode, group)
         # reversed project (FBI backward pass): orders topological on the reverse graph
         rev = orders[:, ::-1].copy()
         for mode in (0, 1):
-            want_c, want_s = oracle.evaluate_batch(inst, rev, mode, reverse=True)
+            want_c, want_s = _oracle_parallel(inst, rev, mode, reverse=True)
             got_c, got_s = device.eval_batch(inst, rev, mode, reverse=True)
             assert np.array_equal(got_c, want_c) and np.array_equal(got_s, want_s)
+
+
+@pytest.mark.parametrize("cfg", FUZZ_CONFIGS)
+def test_eval_fuzz_vs_oracle(cfg):
+    """10^4 precedence-feasible orders per config (2 instances x 5000; Gen-R
+    and the benchmarked Gen-P), both modes, every group size, start times
+    included; plus reversed-project evaluation."""
+    _fuzz(cfg, 5000, 2, GROUPS, CAP_GROUPS, 5)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", FUZZ_CONFIGS)
+def test_eval_fuzz_1e5_vs_oracle(cfg):
+    """10^5 orders per config (4 instances x 25000), both modes, the search's
+    evaluator groups (TIME 32, CAPACITY 32 and 1), starts included."""
+    _fuzz(cfg, 25000, 4, (32,), CAP_GROUPS, 6)
 
 
 def test_eval_fuzz_small_shapes():
@@ -156,7 +182,7 @@ def _check_neighbourhood(inst, orders, mode, delta, group, key):
             assert got.tolist() == want.tolist(), (key, b)
 
 
-@pytest.mark.parametrize("cfg", ["j30", "j60", "j120", "act300"])
+@pytest.mark.parametrize("cfg", ["j30", "j60", "j120", "act300", "j30p", "j60p", "j120p"])
 def test_neighbourhood_makespans_vs_oracle(cfg):
     """Prefix-reusing (group 32) and full-SGS (group 16) neighbourhood
     evaluation inside the search kernel, every move checked."""

@@ -100,3 +100,32 @@ def test_state_ops_fuzz_vs_oracle():
             oracle.time_update(inst, to, act, st)
             assert (ts.free == to).all(), (seed, act)
             starts_t[act] = st
+
+
+def test_cap_update_closed_form_random_rows():
+    """Alg. 4 on arbitrary descending rows -- runs of equal entries, rows
+    longer than a warp (up to 120 entries), demands above 32 -- through
+    rcpsp_state_op (the SGS's warp-wide closed form, sgs.cuh:cap_update_warp)
+    against the reference's loop (oracle.cap_update, kernels.py:81-110).
+    Starts are at or above the Eq. 7 bound, as the SGS guarantees."""
+    rng = np.random.default_rng(11)
+    for trial in range(400):
+        cap = int(rng.choice([3, 17, 40, 75, 120]))
+        m = int(rng.integers(1, 4))
+        caps = [cap] + [int(rng.integers(1, cap + 1)) for _ in range(m - 1)]
+        dur = int(rng.integers(1, 13))
+        dem = [int(rng.integers(1, c + 1)) if rng.random() < 0.8 else 0 for c in caps]
+        inst = make_instance("row", [0, dur, 0], caps, [[0] * m, dem, [0] * m],
+                             [[1], [2], []])
+        st = CapacityResourceState(inst)
+        hi = int(rng.choice([2, 6, 40]))
+        for k, c in enumerate(caps):
+            st.levels[k, :c] = np.sort(rng.integers(0, hi + 1, c))[::-1]
+        ref = st.levels.copy()
+        es = cap_earliest_start(st, 1, inst)
+        assert es == oracle.cap_earliest_start(inst, ref, 1)
+        s = es + int(rng.choice([0, 0, 1, 3]))
+        cap_update(st, 1, s, inst)
+        oracle.cap_update(inst, ref, 1, s)
+        assert (st.levels == ref).all(), (trial, caps, dem, dur, s)
+        assert st.rows_descending()
