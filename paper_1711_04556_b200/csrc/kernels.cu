@@ -658,6 +658,14 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
       }
       entry = -1;
       improved = 0;
+      // the reference's pool-min invariant after every write-back
+      // (WorkingSet._assert_pool_min, cooperation.py:76-79, called by exchange)
+      __syncthreads();
+      bool above = false;
+      for (int i = tid; i < F; i += blockDim.x)
+        above |= static_cast<long long>(__ldcg(&A.ent_cmax[static_cast<size_t>(iid) * F + i])) <
+                 ldcg64(&Hd[WS_BEST]);
+      if (__syncthreads_or(above) && tid == 0) set_err(A.err, DE_POOL_MIN);
     }
     if (tid == 0) {
       const long long best = ldcg64(&Hd[WS_BEST]);
@@ -846,6 +854,11 @@ __global__ void k_merge_elites(RcpspSolveArgs A, const int* elites, const int* e
     __syncthreads();
   }
   if (threadIdx.x == 0 && Hd[WS_BEST] <= Hd[WS_FLOOR]) Hd[WS_STOP] = 1;
+  __syncthreads();
+  bool above = false;
+  for (int i = threadIdx.x; i < F; i += blockDim.x)
+    above |= A.ent_cmax[static_cast<size_t>(iid) * F + i] < Hd[WS_BEST];
+  if (__syncthreads_or(above) && threadIdx.x == 0) set_err(A.err, DE_POOL_MIN);
 }
 
 // =========================================================================

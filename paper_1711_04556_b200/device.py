@@ -395,7 +395,8 @@ def smem_bandwidth(iters: int = 4096, reps: int = 5) -> float:
 
 DEV_ERRORS = {1: "bad instance blob", 2: "no resource window before the horizon "
               "(demand above capacity?)", 3: "shared memory plan", 4: "tabu move outside the "
-              "delta band", 5: "precedence cycle", 6: "bad move"}
+              "delta band", 5: "precedence cycle", 6: "bad move",
+              7: "pool-min invariant violated: global best above a pool entry"}
 
 
 def _raise_dev_err(err) -> None:
