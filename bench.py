@@ -57,9 +57,15 @@ def parse():
                          "(PAPER.md:772)")
     ap.add_argument("--workers", type=int, default=2, help="CTAs (search workers) per instance")
     ap.add_argument("--iters", type=int, default=1000, help="I_total per instance")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "epochs"],
+                    help="N > 1 elite exchange: 'peer' = live, the search kernels read each "
+                         "other's outboxes over peer memory (CUDA IPC / NVLink), no pause; "
+                         "'epochs' = all_gather between search epochs (drains the GPU)")
     ap.add_argument("--epochs", type=int, default=2,
-                    help="search epochs with an elite exchange between them (N > 1); every "
-                         "epoch boundary drains the GPU once")
+                    help="search epochs with an elite exchange between them (--exchange "
+                         "epochs, N > 1)")
+    ap.add_argument("--poll-every", type=int, default=4,
+                    help="--exchange peer: exchanges of a worker between outbox polls")
     ap.add_argument("--group", type=int, default=None, help="TIME lanes per schedule")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = auto)")
     ap.add_argument("--mode", default="rule", choices=["rule", "time", "capacity"],
@@ -430,10 +436,21 @@ def main() -> None:
     solver.upload()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")  # > L2
-    epochs = args.epochs if ws > 1 else 1
     n_max = solver.n_max
     I = len(insts)
-    exchange = EliteExchange(solver, I, n_max) if ws > 1 else None
+    exchange, peer, xmode, xnote = None, None, "none", None
+    if ws > 1 and args.exchange == "peer":
+        try:
+            from paper_1711_04556_b200.population import PeerExchange
+            peer = PeerExchange(solver, poll_every=args.poll_every)
+            solver.peer = peer
+            xmode = "peer"
+        except Exception as exc:  # e.g. no CUDA IPC between the ranks' devices
+            xnote = f"peer exchange unavailable ({type(exc).__name__}: {exc}); epochs used"
+    if ws > 1 and peer is None:
+        exchange = EliteExchange(solver, I, n_max)
+        xmode = "epochs"
+    epochs = args.epochs if xmode == "epochs" else 1
 
     def one_step(timed_search: list | None = None) -> None:
         solver.pool_init(stream)
@@ -482,6 +499,7 @@ def main() -> None:
                                       / res.critical_path)))
     launches = solver.launches - launches0
     clk = clocks.summary()
+    peer_counters = peer.counters() if peer is not None else None
 
     # whole-job aggregation: evaluations summed over ranks, time = max over ranks
     tot_ms = sum(step_ms)
@@ -522,6 +540,9 @@ def main() -> None:
         e_ev = int(ee.item())
     e2e = e_ev / e_t if e_t > 0 else 0.0
 
+    if peer is not None:
+        dist.barrier()          # nobody unmaps an outbox a peer may still read
+        peer.close()
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -549,7 +570,11 @@ def main() -> None:
         if rec:
             traffic = rec["dram_bytes_per_schedule"] * search_evals / (args.steps * epochs)
 
-    if ws > 1:
+    if xmode == "peer":
+        par = (f"{ws} independent search populations (one per GPU), live elite exchange: "
+               f"search kernels read each other's outboxes over peer memory (CUDA IPC), "
+               f"poll every {args.poll_every} exchanges; {backend} for the host plumbing")
+    elif xmode == "epochs":
         par = (f"{ws} independent search populations (one per GPU), elite exchange "
                f"between {epochs} epochs by all_gather over {backend}")
     else:
@@ -563,7 +588,9 @@ def main() -> None:
         "run": {"workers_per_instance": args.workers, "epochs": epochs,
                 "cpm_dev": float(np.mean(devs)), "evaluations_per_step": evals // args.steps,
                 "iterations_per_step": iters_done // args.steps,
-                "l2": "256 MiB buffer written between timed steps", "parallelism": par},
+                "l2": "256 MiB buffer written between timed steps", "parallelism": par,
+                "exchange": xmode, **({"exchange_note": xnote} if xnote else {}),
+                **({"peer_counters_last_step": peer_counters} if peer is not None else {})},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "kernel": "k_solve", "bytes_per_schedule": bytes_per_sched,

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define RCPSP_ABI_VERSION 7
+#define RCPSP_ABI_VERSION 8
 
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
@@ -53,9 +53,9 @@ typedef struct RcpspSolveArgs {
     int64_t total_iters;        /* I_total per instance                   */
     int64_t block_iters;        /* ceil(I_total / B) (search.py:39-42)    */
     int64_t epoch_limit;        /* planned-iteration limit of this launch */
-    int64_t grant_cap;          /* 0 = uncapped (cooperation.py:317)      */
+    int64_t grant_cap;          /* 0 = uncapped (cooperation.py:123-124)      */
     int64_t collect_trace;      /* 1 = write per-iteration traces         */
-    /* working set (cooperation.py:246-273), per instance */
+    /* working set (cooperation.py:52-80, 253-273), per instance */
     int32_t *ws_lock;           /* [I]                                    */
     int64_t *ws_hdr;            /* [I*16] see WS_* in kernels.cu          */
     int32_t *ent_order;         /* [I*F*n_max]                            */
@@ -105,7 +105,23 @@ typedef struct RcpspSolveArgs {
                                  * initialised default) is always safe.  A
                                  * violated guarantee is caught on the device
                                  * (DE_SMEM) instead of corrupting memory. */
+    /* live elite exchange between independent populations over peer memory
+     * (ABI 8; all NULL / 0 = off).  Each population publishes its
+     * per-instance global best in its outbox (seqlock: seq odd while being
+     * written) and, every poll_every exchanges of a worker, reads the other
+     * populations' outboxes directly (CUDA IPC mappings: P2P loads over
+     * NVLink/NVSwitch), importing the best new foreign elite into the worst
+     * pool entry -- no host round trip, no pause of the search. */
+    int32_t *outbox;            /* [I * RCPSP_OUTBOX_WORDS(n_max)] own, or NULL */
+    const int64_t *peers;       /* [n_peers] device addresses of peer outboxes */
+    int64_t n_peers;            /* <= 32 */
+    int32_t *peer_seen;         /* [I * n_peers] last sequence imported per peer */
+    int64_t poll_every;         /* exchanges between polls (>= 1) */
+    int64_t *peer_stats;        /* [4]: imports, publishes, polls, torn reads */
 } RcpspSolveArgs;
+
+/* words of one instance's outbox: seq, cmax, 2 reserved, order[n_max] */
+#define RCPSP_OUTBOX_WORDS(n_max) (4 + (n_max))
 
 /* Shape of one packed instance (the blob header), what the host needs to size
  * a launch without reading device memory. */
@@ -152,9 +168,9 @@ const char *rcpsp_pack_last_error(void);
 int rcpsp_device_info(int *sm_count, int *smem_optin, int *cc_major, int *cc_minor);
 
 /* Batch of evaluate_order calls (kernels.py:152-194; evaluator.evaluate
- * evaluator.py:230-246).  orders: [B*n] precedence-feasible permutations.
+ * evaluator.py:128-144).  orders: [B*n] precedence-feasible permutations.
  * reverse != 0 evaluates the time-reversed project (successor lists used as
- * predecessor lists, evaluator.py:336-344).  cmax: [B]; starts: [B*n] or
+ * predecessor lists, evaluator.py:234-242).  cmax: [B]; starts: [B*n] or
  * NULL.  group: TIME lanes per schedule (32/16/8). */
 int rcpsp_eval_batch(const int32_t *blob, const RcpspShape *shape, int mode, const int32_t *orders, int batch,
                      int reverse, int32_t *cmax, int32_t *starts, int group, int32_t *err,
@@ -182,10 +198,10 @@ int rcpsp_run_chunk_batch(const int32_t *blob, const RcpspShape *shape, int mode
                           int32_t *cmax_buf, int nbhd_max, int group, int threads, int32_t *err,
                           void *stream);
 
-/* initialize_working_set (cooperation.py:332-354) for the instances listed in
+/* initialize_working_set (cooperation.py:138-160) for the instances listed in
  * inst_ids: level-shuffled orders from the pool PCG64 state (one state per
  * instance, 6 words each: default_rng(seed)), forward-backward improvement
- * of even entries (evaluator.py:309-368), evaluation, global best. */
+ * of even entries (evaluator.py:207-266), evaluation, global best. */
 int rcpsp_pool_init(const RcpspSolveArgs *args, const int32_t *inst_ids, int n_ids, int mode,
                     const uint64_t *pool_rng, void *stream);
 
@@ -204,6 +220,15 @@ int rcpsp_solve(const RcpspSolveArgs *args, const int32_t *inst_ids, int n_ids, 
 int rcpsp_merge_elites(const RcpspSolveArgs *args, const int32_t *elites,
                        const int32_t *elite_cmax, int n_src, void *stream);
 
+/* Outboxes of the live exchange: cudaMalloc'd (the IPC handle of an
+ * allocation names its base), zeroed; handle: 64 bytes (cudaIpcMemHandle_t)
+ * for the peers, which map it with rcpsp_outbox_open (P2P enabled lazily). */
+int rcpsp_outbox_alloc(int64_t bytes, void **dev_ptr, void *handle);
+int rcpsp_outbox_open(const void *handle, void **dev_ptr);
+int rcpsp_outbox_close(void *dev_ptr);
+int rcpsp_outbox_free(void *dev_ptr);
+int rcpsp_outbox_reset(void *dev_ptr, int64_t bytes, void *stream);  /* zero, async */
+
 /* Export each instance's global best (order, cmax) into [I*n_max] / [I]. */
 int rcpsp_export_elites(const RcpspSolveArgs *args, int32_t *elites, int32_t *elite_cmax,
                         void *stream);
@@ -214,7 +239,7 @@ int rcpsp_diversify_batch(const int32_t *blob, const RcpspShape *shape, int32_t 
                           int batch, int phi_steps, uint64_t *rng, int32_t *err, void *stream);
 
 /* Single-step resource-state operations on the reference's state layouts
- * (kernels.py:68-146 via evaluator.py:171-209): op 0 = cap_earliest_start,
+ * (kernels.py:68-146 via evaluator.py:69-107): op 0 = cap_earliest_start,
  * 1 = cap_update (arg = start), 2 = time_earliest_start (arg = es_prec),
  * 3 = time_update (arg = start).  state: CAP int32 [m][R_max], TIME int32
  * [m][H+1] (updated in place); out[0] receives the earliest start. */
@@ -222,7 +247,7 @@ int rcpsp_state_op(const int32_t *blob, const RcpspShape *shape, int op, int32_t
                    int32_t *err, void *stream);
 
 /* Parity probes of the device RNG and Eq. 8 (assigned_iterations,
- * cooperation.py:233-243). ops: [k*2] (kind, n) with kind 0 = integers(n),
+ * cooperation.py:39-49). ops: [k*2] (kind, n) with kind 0 = integers(n),
  * 1 = permutation(arange(n)); out receives the draws back to back. */
 int rcpsp_rng_probe(uint64_t *state, const int32_t *ops, int k, int32_t *out, void *stream);
 /* Shared-memory bandwidth microbenchmark (the roofline denominator of the

@@ -224,7 +224,7 @@ def run_chunk(inst, order, tabu_list, tabu_head, budget, adopted_cmax, start_cma
 
 
 def fbi(inst, order, mode: int):
-    """forward_backward_improve (evaluator.py:309-368): (order, starts, cmax, evals)."""
+    """forward_backward_improve (evaluator.py:207-266): (order, starts, cmax, evals)."""
     oi = _oi(inst)
     fo = np.zeros(oi.n, np.int32)
     fs = np.zeros(oi.n, np.int32)
@@ -267,7 +267,7 @@ def size_defaults(n: int):
 def orchestrate(inst, total_iters: int, workers: int = 1, seed: int = 0, mode: int = MODE_TIME,
                 delta: int | None = None, tabu_size: int | None = None, phi_steps: int = 20,
                 phi_max: int = 3, pool_size: int = 16, collect_trace: bool = False) -> dict:
-    """cooperation.orchestrate (cooperation.py:431-496) with a pinned mode."""
+    """cooperation.orchestrate (cooperation.py:237-302) with a pinned mode."""
     oi = _oi(inst)
     d0, t0 = size_defaults(oi.n)
     delta = d0 if delta is None else delta

@@ -272,7 +272,7 @@ static void inst_fill(oinst_t *I, int n, int m, int horizon, const int32_t *dur,
 
 /* Batch evaluation: B orders (B x n) -> cmax[B] (+ starts B x n if non-NULL).
  * `use_succ` evaluates on the reversed project (preds = successor lists), as
- * forward_backward_improve's eval_backward does (evaluator.py:336-344). */
+ * forward_backward_improve's eval_backward does (evaluator.py:234-242). */
 int oracle_evaluate_batch(int n, int m, int horizon, const int32_t *dur, const int32_t *dem,
                           const int32_t *cap, const int32_t *pred_ptr, const int32_t *pred_dat,
                           const int32_t *succ_ptr, const int32_t *succ_dat, const int32_t *orders,
@@ -543,9 +543,9 @@ int oracle_run_chunk(int n, int m, int horizon, const int32_t *dur, const int32_
 }
 
 /* ------------------------------------------------------------------------ */
-/* Forward-backward improvement (evaluator.py:289-368).                      */
+/* Forward-backward improvement (evaluator.py:187-266).                      */
 
-/* evaluator.py:289-306: topological order preferring small key, ties by id.
+/* evaluator.py:187-205: topological order preferring small key, ties by id.
  * key2[i] is the primary key; (key2[i], i) is unique so a selection scan is
  * equivalent to the reference's heap.  The graph is given as CSR `nxt` (the
  * "successors" in the traversal direction) and in-degree array indeg0. */
@@ -569,7 +569,7 @@ static int priority_topo(int n, const int32_t *nxt_ptr, const int32_t *nxt_dat,
     return filled == n ? 0 : -1;
 }
 
-/* evaluator.py:309-368 ; writes final order and starts, returns cmax */
+/* evaluator.py:207-266 ; writes final order and starts, returns cmax */
 static int fbi_raw(const oinst_t *I, const int32_t *order_in, int mode, oscratch_t *S,
                    int32_t *final_order, int32_t *final_starts) {
     int n = I->n;
@@ -678,7 +678,7 @@ typedef struct {
     long n_chunks, chunk_cap;
 } oworker_t;
 
-/* cooperation.py:233-243 (Eq. 8, quantity term read as I_block/5) */
+/* cooperation.py:39-49 (Eq. 8, quantity term read as I_block/5) */
 long oracle_assigned_iterations(int cmax, long ic, long block_iters, int best_cmax) {
     double quality = 0.8 * exp(-100.0 * ((double)cmax / (double)best_cmax - 1.0));
     double intact = 0.2 * exp(-4.0 * ((double)ic / (double)block_iters));
@@ -697,7 +697,7 @@ static void tabu_load(oworker_t *w, const int32_t *entries, int head) {
     w->tabu_head = head % T;
 }
 
-/* cooperation.py:276-329 ; returns 1 with an adoption, 0 when the run is over */
+/* cooperation.py:82-135 ; returns 1 with an adoption, 0 when the run is over */
 static int exchange(oworker_t *w, ows_t *ws, long *grant_out, int *best_known, int *needs_div) {
     int n = w->I->n, T = w->P->T;
     pthread_mutex_lock(&ws->lock);
@@ -888,7 +888,7 @@ int oracle_critical_path(int n, const int32_t *dur, const int32_t *pred_ptr,
     return cpm_of(&I);
 }
 
-/* Full orchestrate (cooperation.py:431-496) without the dynamic-mode
+/* Full orchestrate (cooperation.py:237-302) without the dynamic-mode
  * controller.  params7 = {total_iters, workers, delta, tabu_size, phi_steps,
  * phi_max, pool_size}; seeds = 6 uint64 per PCG64 state: [0] is the pool
  * rng default_rng(seed), [1 + w] is worker w's default_rng(seed ^ w).
@@ -930,7 +930,7 @@ int oracle_orchestrate(int n, int m, int horizon, const int32_t *dur, const int3
     int32_t *moves_all = gen_neighborhood(n, P.delta, &n_all);
 
     double tick = now_s();
-    /* initialize_working_set (cooperation.py:332-354) */
+    /* initialize_working_set (cooperation.py:138-160) */
     pcg64_t pool_rng;
     pcg_load(&pool_rng, seeds);
     oscratch_t S0;

@@ -19,7 +19,7 @@ LIB_PATH = _HERE / "_lib" / "libb200tabu.so"
 # A/B measurements of kernel variants (tools/ab_bench.sh) point this at another build
 if os.environ.get("RCPSP_B200_LIB"):
     LIB_PATH = Path(os.environ["RCPSP_B200_LIB"])
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _lib = None
 
@@ -52,6 +52,8 @@ class RcpspSolveArgs(ctypes.Structure):
         ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
         ("cluster", ctypes.c_int64), ("time_budget_ns", ctypes.c_int64), ("t0_ns", _vp),
         ("no_big", ctypes.c_int64),
+        ("outbox", _vp), ("peers", _vp), ("n_peers", ctypes.c_int64), ("peer_seen", _vp),
+        ("poll_every", ctypes.c_int64), ("peer_stats", _vp),
     ]
 
 
@@ -82,6 +84,11 @@ _SIGNATURES = {
     "rcpsp_solve": ([ctypes.POINTER(RcpspSolveArgs), _vp, _i, _i, _vp], _i),
     "rcpsp_merge_elites": ([ctypes.POINTER(RcpspSolveArgs), _vp, _vp, _i, _vp], _i),
     "rcpsp_export_elites": ([ctypes.POINTER(RcpspSolveArgs), _vp, _vp, _vp], _i),
+    "rcpsp_outbox_alloc": ([ctypes.c_int64, ctypes.POINTER(_vp), _vp], _i),
+    "rcpsp_outbox_open": ([_vp, ctypes.POINTER(_vp)], _i),
+    "rcpsp_outbox_close": ([_vp], _i),
+    "rcpsp_outbox_free": ([_vp], _i),
+    "rcpsp_outbox_reset": ([_vp, ctypes.c_int64, _vp], _i),
     "rcpsp_diversify_batch": ([_vp, _SHP, _vp, _i, _i, _vp, _vp, _vp], _i),
     "rcpsp_rng_probe": ([_vp, _vp, _i, _vp, _vp], _i),
     "rcpsp_eq8_probe": ([_vp, _i, _vp, _vp], _i),

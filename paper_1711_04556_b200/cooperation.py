@@ -40,7 +40,7 @@ class WorkingSetEntry:
 
 
 def assigned_iterations(entry: WorkingSetEntry, block_iters: int, best_cmax: int) -> int:
-    """Eq. 8 with the quantity term read as block_iters/5 (cooperation.py:233-243).
+    """Eq. 8 with the quantity term read as block_iters/5 (cooperation.py:39-49).
 
     The device evaluates the same expression in double precision
     (csrc/kernels.cu:eq8); tests/test_gpu_parity.py pins the two together."""
@@ -79,7 +79,7 @@ class WorkingSet:
 
 
 def exchange(worker: Worker, ws: WorkingSet):
-    """Write back, then adopt the next entry round-robin (cooperation.py:276-329).
+    """Write back, then adopt the next entry round-robin (cooperation.py:82-135).
     Returns (order copy, grant, best-known cmax, diversify flag) or None."""
     with ws.lock:
         if worker.entry_index >= 0:
@@ -213,7 +213,7 @@ class RunStats:
 
 def choose_mode(instance: ProjectInstance, params: SearchParams, requested: str,
                 rules=DEFAULT_RULES) -> tuple[EvalMode, DynamicModeController | None]:
-    """Resolve an --eval request (cooperation.py:398-419)."""
+    """Resolve an --eval request (cooperation.py:204-225)."""
     if requested == "capacity":
         return EvalMode.CAPACITY, None
     if requested == "time":
@@ -254,7 +254,7 @@ def _finish(instance: ProjectInstance, res: device.BatchResult, i: int, params: 
 def orchestrate(instance: ProjectInstance, params: SearchParams, mode: EvalMode | None = None,
                 mode_controller: DynamicModeController | None = None,
                 time_limit_s: float | None = None) -> RunStats:
-    """Solve one instance on the GPU with `params.workers` CTAs (cooperation.py:431-496).
+    """Solve one instance on the GPU with `params.workers` CTAs (cooperation.py:237-302).
 
     With B = 1 and a pinned mode the trajectory (trace, evaluations,
     exchanges, best) is identical to the reference.  A dynamic controller

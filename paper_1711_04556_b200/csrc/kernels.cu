@@ -2,9 +2,9 @@
 //
 // K1 k_eval_batch   evaluate_order over a batch of orders (kernels.py:152-194)
 // K2 k_run_chunk    run_chunk, one CTA per independent search (kernels.py:316-385)
-// K0 k_pool_*       initialize_working_set + FBI (cooperation.py:332-354,
-//                   evaluator.py:289-368), one warp per pool entry
-// K3 k_solve        persistent search: exchange (cooperation.py:276-329) +
+// K0 k_pool_*       initialize_working_set + FBI (cooperation.py:138-160,
+//                   evaluator.py:187-266), one warp per pool entry
+// K3 k_solve        persistent search: exchange (cooperation.py:82-135) +
 //                   diversify (search.py:77-94) + run_adopted (search.py:144-173)
 //                   per CTA, the working set in HBM behind a per-instance lock
 // K4 k_merge_elites elite exchange between independent populations (multi-GPU)
@@ -252,7 +252,7 @@ __global__ void k_rng_probe(uint64_t* state, const int* ops, int k, int* out) {
   g.store(state);
 }
 
-// Eq. 8, cooperation.py:233-243 (same double-precision operation order)
+// Eq. 8, cooperation.py:39-49 (same double-precision operation order)
 __device__ __forceinline__ long long eq8(long long cmax, long long ic, long long block_iters,
                                          long long best) {
   const double quality = 0.8 * exp(-100.0 * (static_cast<double>(cmax) / static_cast<double>(best) - 1.0));
@@ -399,7 +399,7 @@ __device__ __forceinline__ int warp_eval(const SInst& I, int* scr, const int* or
   return cm;
 }
 
-// _priority_topo (evaluator.py:289-306) by one warp: repeatedly emit the
+// _priority_topo (evaluator.py:187-205) by one warp: repeatedly emit the
 // ready activity with the smallest (key, id).  deg_ptr gives the in-degree.
 __device__ bool warp_ptopo(int n, const int* nxt_ptr, const int* nxt_dat, const int* deg_ptr,
                            const int* key, int* out, int* indeg, int* ready) {
@@ -447,8 +447,8 @@ __host__ __device__ inline int pool_entry_words(int mode, int n, int m, int H, i
   return inst + arrays + ev + 8;
 }
 
-// forward_backward_improve (evaluator.py:309-368) for even entries, then the
-// evaluation of every entry (cooperation.py:340-351); one warp per entry.
+// forward_backward_improve (evaluator.py:207-266) for even entries, then the
+// evaluation of every entry (cooperation.py:146-157); one warp per entry.
 template <int MODE, int W>
 __global__ void __launch_bounds__(32) k_pool_entry(RcpspSolveArgs A, const int* ids) {
   int* smem = dsm;
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(32) k_pool_entry(RcpspSolveArgs A, const int* 
   }
 }
 
-// WorkingSet.__init__ (cooperation.py:249-268)
+// WorkingSet.__init__ (cooperation.py:55-74)
 __global__ void k_pool_finalize(RcpspSolveArgs A, const int* ids, int n_ids, int mode) {
   const int slot = blockIdx.x;
   if (slot >= n_ids) return;
@@ -552,6 +552,125 @@ __device__ __forceinline__ int64_t ldcg64(const int64_t* p) {
 
 __device__ __forceinline__ void add64(int64_t* p, long long v) {
   atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// ---- live elite exchange over peer memory (RcpspSolveArgs.outbox / peers)
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_volatile_g(const int32_t* p) {
+  int v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Publish this population's new global best of instance iid (all threads;
+// caller holds the instance lock, so there is one writer per outbox).
+// Seqlock: seq odd while the order is being written, even once complete.
+__device__ void publish_best(const RcpspSolveArgs& A, int iid, const int* best, int n, int cmax) {
+  volatile int32_t* ob = A.outbox + static_cast<size_t>(iid) * RCPSP_OUTBOX_WORDS(A.n_max);
+  const int tid = threadIdx.x;
+  if (tid == 0) ob[0] = ob[0] + 1;
+  __threadfence_system();
+  __syncthreads();
+  for (int p = tid; p < n; p += blockDim.x) ob[4 + p] = best[p];
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    ob[1] = cmax;
+    __threadfence_system();
+    ob[0] = ob[0] + 1;
+    __threadfence_system();
+    if (A.peer_stats) atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[1]), 1ull);
+  }
+  __syncthreads();
+}
+
+// Import the best new foreign elite of instance iid, if it beats the pool's
+// worst entry and its makespan is not in the pool yet (k_merge_elites' rule):
+// the entry takes the order, its tabu list is cleared, IC and reads reset,
+// and the global best follows.  Warp 0 works (one peer per lane, n_peers <=
+// 32), the CTA waits; `stage` is free shared scratch of n words.  Caller
+// holds the instance lock.
+template <int MODE>
+__device__ void import_peer_elite(const RcpspSolveArgs& A, int iid, int n, int* stage,
+                                  int64_t* Hd) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int np = static_cast<int>(A.n_peers), F = static_cast<int>(A.pool_size),
+            T = static_cast<int>(A.tabu_size);
+  const size_t W = RCPSP_OUTBOX_WORDS(A.n_max);
+  if (tid < 32) {
+    int seq = 0;
+    unsigned key = 0xffffffffu;
+    const int32_t* pob = nullptr;
+    if (lane < np) {
+      pob = reinterpret_cast<const int32_t*>(A.peers[lane]) + static_cast<size_t>(iid) * W;
+      seq = ld_acquire_sys(pob);
+      const int cm = ld_volatile_g(pob + 1);
+      const int seen = A.peer_seen[static_cast<size_t>(iid) * np + lane];
+      if (seq != 0 && !(seq & 1) && seq != seen) key = (static_cast<unsigned>(cm) << 5) | lane;
+    }
+    const unsigned best = __reduce_min_sync(FULL_MASK, key);
+    if (best != 0xffffffffu) {
+      const int src = static_cast<int>(best & 31u), ccm = static_cast<int>(best >> 5);
+      const int sseq = __shfl_sync(FULL_MASK, seq, src);
+      const int32_t* sob = reinterpret_cast<const int32_t*>(
+          __shfl_sync(FULL_MASK, reinterpret_cast<unsigned long long>(pob), src));
+      // the pool's worst entry (lowest index on ties) and the duplicate test
+      unsigned wkey = 0;
+      bool dup = false;
+      for (int i = lane; i < F; i += 32) {
+        const int v = __ldcg(&A.ent_cmax[static_cast<size_t>(iid) * F + i]);
+        dup |= v == ccm;
+        const unsigned k = (static_cast<unsigned>(v) << 16) | static_cast<unsigned>(0xffff - i);
+        wkey = k > wkey ? k : wkey;
+      }
+      dup = __any_sync(FULL_MASK, dup);
+      wkey = __reduce_max_sync(FULL_MASK, wkey);
+      const int worst_c = static_cast<int>(wkey >> 16), worst = 0xffff - static_cast<int>(wkey & 0xffffu);
+      bool imported = false;
+      if (!dup && ccm < worst_c) {
+        for (int p = lane; p < n; p += 32) stage[p] = ld_volatile_g(sob + 4 + p);
+        __threadfence_system();
+        __syncwarp();
+        const int seq2 = __shfl_sync(FULL_MASK, lane == 0 ? ld_acquire_sys(sob) : 0, 0);
+        if (seq2 == sseq) {  // not overwritten meanwhile: a consistent order
+          const size_t eo = static_cast<size_t>(iid) * F + worst;
+          for (int p = lane; p < n; p += 32) A.ent_order[eo * A.n_max + p] = stage[p];
+          for (int i = lane; i < T; i += 32) A.ent_tabu[eo * T + i] = 0u;
+          const bool gb = ccm < ldcg64(&Hd[WS_BEST]);
+          if (gb)
+            for (int p = lane; p < n; p += 32)
+              A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] = stage[p];
+          if (lane == 0) {
+            A.ent_cmax[eo] = ccm;
+            A.ent_head[eo] = 0;
+            A.ent_ic[eo] = 0;
+            A.ent_reads[eo] = 0;
+            if (gb) {
+              Hd[WS_BEST] = ccm;
+              Hd[WS_BEST_MODE] = MODE;
+            }
+          }
+          imported = true;
+        } else if (lane == 0 && A.peer_stats) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[3]), 1ull);
+        }
+      }
+      // a consistent elite is consumed whether or not it entered the pool
+      if (lane == 0 && (imported || dup || ccm >= worst_c)) {
+        A.peer_seen[static_cast<size_t>(iid) * np + src] = sseq;
+        if (imported && A.peer_stats)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[0]), 1ull);
+      }
+    }
+    if (lane == 0 && A.peer_stats)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[2]), 1ull);
+    __syncwarp();
+  }
+  __syncthreads();
 }
 
 // One CTA = one search worker.  Worker loop (search.run_worker): exchange
@@ -618,10 +737,10 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
   int64_t* Hd = A.ws_hdr + static_cast<size_t>(iid) * 16;
   if (tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(&Hd[WS_T0]), globaltimer());
   int entry = -1, improved = 0, local_best = 0;
-  long long granted = 0, used = 0;
+  long long granted = 0, used = 0, polls = 0;
   int hops = 0;
   for (;;) {
-    // ---------------- exchange (cooperation.py:276-329), under the lock
+    // ---------------- exchange (cooperation.py:82-135), under the lock
     if (tid == 0) {
       while (atomicCAS(&A.ws_lock[iid], 0, 1) != 0) __nanosleep(100);
       __threadfence();
@@ -641,6 +760,8 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
         }
       }
       __syncthreads();
+      if (A.outbox && improved && local_best < gbest)
+        publish_best(A, iid, c.best, c.I.n, local_best);
       if (tid == 0) {
         const long long unused = granted - used;
         Hd[WS_PLANNED] = ldcg64(&Hd[WS_PLANNED]) - (unused > 0 ? unused : 0);
@@ -667,6 +788,10 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
                  ldcg64(&Hd[WS_BEST]);
       if (__syncthreads_or(above) && tid == 0) set_err(A.err, DE_POOL_MIN);
     }
+    // live elite exchange: poll the other populations' outboxes (c.best is
+    // free here: the write-back above has consumed it)
+    if (A.n_peers > 0 && ++polls % A.poll_every == 0)
+      import_peer_elite<MODE>(A, iid, c.I.n, c.best, Hd);
     if (tid == 0) {
       const long long best = ldcg64(&Hd[WS_BEST]);
       if (best <= ldcg64(&Hd[WS_FLOOR])) Hd[WS_STOP] = 1;
@@ -1147,6 +1272,9 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   if (threads % 32 || threads < 0 || threads > KSOLVE_THREADS_MAX)
     return fail("threads must be 0 (auto) or 32.." + std::to_string(KSOLVE_THREADS_MAX) + ", x32");
   if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
+  if (A.n_peers < 0 || A.n_peers > 32) return fail("n_peers must be 0..32");
+  if (A.n_peers > 0 && (A.peers == nullptr || A.peer_seen == nullptr || A.poll_every < 1))
+    return fail("peer exchange needs peers, peer_seen and poll_every >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return dispatch(mode, static_cast<int>(A.group), static_cast<int>(A.words), static_cast<int>(A.m_max),
                   [&]<int MODE, int G, int W>() -> int {
@@ -1191,6 +1319,36 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
       return -1;
     return launch_check("k_solve");
   });
+}
+
+int rcpsp_outbox_alloc(int64_t bytes, void** dev_ptr, void* handle) {
+  if (bytes <= 0 || dev_ptr == nullptr || handle == nullptr) return fail("bad outbox request");
+  if (cuda_check(cudaMalloc(dev_ptr, static_cast<size_t>(bytes)), "cudaMalloc(outbox)")) return -1;
+  if (cuda_check(cudaMemset(*dev_ptr, 0, static_cast<size_t>(bytes)), "cudaMemset(outbox)"))
+    return -1;
+  cudaIpcMemHandle_t h;
+  if (cuda_check(cudaIpcGetMemHandle(&h, *dev_ptr), "cudaIpcGetMemHandle")) return -1;
+  std::memcpy(handle, &h, sizeof(h));
+  return 0;
+}
+
+int rcpsp_outbox_open(const void* handle, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cuda_check(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                    "cudaIpcOpenMemHandle");
+}
+
+int rcpsp_outbox_close(void* dev_ptr) {
+  return cuda_check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+}
+
+int rcpsp_outbox_free(void* dev_ptr) { return cuda_check(cudaFree(dev_ptr), "cudaFree(outbox)"); }
+
+int rcpsp_outbox_reset(void* dev_ptr, int64_t bytes, void* stream) {
+  return cuda_check(cudaMemsetAsync(dev_ptr, 0, static_cast<size_t>(bytes),
+                                    static_cast<cudaStream_t>(stream)),
+                    "cudaMemsetAsync(outbox)");
 }
 
 int rcpsp_export_elites(const RcpspSolveArgs* args, int32_t* elites, int32_t* elite_cmax,

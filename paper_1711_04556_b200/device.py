@@ -531,6 +531,7 @@ class BatchSolver:
         self.d_pool_rng = z((I, 6), i64)
         self.d_ids = {k: z(len(v), i32) for k, v in groups.items()}
         self.launches = 0
+        self.peer = None          # population.PeerExchange (live elite exchange), or None
 
     # -- host -> device inputs (the e2e measurement times this too)
     def upload(self, pinned: bool = False) -> int:
@@ -557,6 +558,8 @@ class BatchSolver:
             t.zero_()
         self.w_rng.copy_(_torch().from_numpy(self.w_rng_host.view(np.int64)).cuda())
         self.t0.fill_(np.iinfo(np.int64).max)
+        if self.peer is not None:
+            self.peer.reset()
         if self.w_trace is not None:
             self.w_trace.zero_()
             self.w_chunks.zero_()
@@ -598,6 +601,8 @@ class BatchSolver:
         a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
         a.no_big = self.no_big
         a.t0_ns = ptr(self.t0)
+        if self.peer is not None:
+            self.peer.fill_args(a)
         return a
 
     def pool_init(self, stream=None) -> None:

@@ -187,7 +187,7 @@ def main() -> None:
                    "out_stats": [int(x) for x in out], "out_tabu_list": tabu.entries.tolist()})
     g["run_chunk"] = rc
 
-    # --- orchestrate, B = 1, pinned mode (cooperation.py:431-496) -----------
+    # --- orchestrate, B = 1, pinned mode (cooperation.py:237-302) -----------
     orch = []
     runs = [("genr30s0", 1000, 0, 1, {}), ("genr30s0", 1000, 0, 0, {}),
             ("example12", 300, 21, 1, {}), ("example12", 2000, 3, 1, {}),
@@ -233,7 +233,7 @@ def main() -> None:
                    "orders": [R.initial_order(inst, True, r).tolist() for _ in range(4)]})
     g["initial_order"] = io
 
-    # --- Eq. 8 (cooperation.py:233-243) --------------------------------------
+    # --- Eq. 8 (cooperation.py:39-49) --------------------------------------
     ai = []
     grid_rng = np.random.default_rng(11)
     for _ in range(400):

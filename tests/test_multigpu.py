@@ -117,3 +117,101 @@ def test_merge_model_semantics():
     # 12 already present -> skipped; 11 replaces 15 (worst); 9 replaces 12, becomes best
     pc, po, b, bo = merge_model(pool_c, pool_o, 10, [0, 1], [[1, 0], [2, 0], [3, 0]], [12, 11, 9])
     assert pc == [10, 9, 11] and b == 9 and bo == [3, 0]
+
+
+# ---------------------------------------------------------------------------
+# the same plumbing with device.BatchSolver: two ranks sharing one GPU (gloo)
+
+def _gpu_worker(rank: int, world: int, port: int, kind: str, out):
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1711_04556_b200 import evaluate, synth
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    from paper_1711_04556_b200.population import PeerExchange
+    insts = synth.benchmark_batch("j60p", 6, first_seed=20)
+    res = {}
+    if kind == "epochs":
+        cfg = SolveConfig(total_iters=200, workers=2, pool_size=8, tabu_size=250, delta=60,
+                          phi_steps=20, phi_max=3, seed=1000 * rank)
+        s = BatchSolver(insts, [1] * 6, cfg)
+        s.upload()
+        s.pool_init()
+        ex = EliteExchange(s, len(insts), s.n_max)
+        run_epochs(s, 200, 4, ex)
+        r = s.collect()
+        res["rounds"] = ex.rounds
+    else:
+        iters = 300 if rank == 1 else 5
+        cfg = SolveConfig(total_iters=iters, workers=1, pool_size=8, tabu_size=250, delta=60,
+                          phi_steps=20, phi_max=3, seed=1000 * rank)
+        s = BatchSolver(insts, [1] * 6, cfg)
+        peer = PeerExchange(s, poll_every=1)
+        s.peer = peer
+        s.upload()
+        s.pool_init()
+        torch.cuda.synchronize()
+        res["pool_worst"] = s.ent_cmax.cpu().numpy().max(1).tolist()
+        res["pool_all"] = s.ent_cmax.cpu().numpy().tolist()
+        if rank == 1:
+            s.search()                 # publishes its improvements
+            torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            s.search()                 # polls rank 1's outbox at its exchanges
+            torch.cuda.synchronize()
+        dist.barrier()
+        r = s.collect()
+        res["counters"] = peer.counters()
+        res["pool_after"] = s.ent_cmax.cpu().numpy().tolist()
+        dist.barrier()                 # nobody unmaps before everyone is done
+        peer.close()
+    res["best"] = r.best_cmax.tolist()
+    res["iters_ok"] = bool(((r.iterations == cfg.total_iters)
+                            | (r.best_cmax == r.critical_path)).all())
+    res["valid"] = [evaluate(r.best_order[i, :x.n_activities], x, 1).cmax == int(r.best_cmax[i])
+                    for i, x in enumerate(insts)]
+    out[rank] = res
+    dist.destroy_process_group()
+
+
+def _spawn_gpu(kind: str):
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gpu_worker, args=(world, port, kind, out), nprocs=world, join=True)
+    return out[0], out[1]
+
+
+@pytest.mark.gpu
+def test_two_rank_epoch_exchange_batchsolver():
+    """Epoch exchange (export -> all_gather -> merge) driving device.BatchSolver:
+    every epoch boundary merges, budgets are kept, bests are valid schedules,
+    and every instance spends its budget (or stops at the critical path)."""
+    r0, r1 = _spawn_gpu("epochs")
+    for r in (r0, r1):
+        assert r["rounds"] == 3
+        assert all(r["valid"])
+        assert r["iters_ok"]
+
+
+@pytest.mark.gpu
+def test_two_rank_peer_exchange():
+    """Live exchange over peer memory (CUDA IPC; two processes on one GPU):
+    rank 1 searches and publishes, rank 0 then polls at its first exchange and
+    imports every foreign elite that beats its pool's worst entry; imported
+    orders are consistent (their evaluation equals the claimed makespan)."""
+    r0, r1 = _spawn_gpu("peer")
+    assert r1["counters"]["publishes"] > 0
+    assert r0["counters"]["polls"] > 0 and r0["counters"]["imports"] > 0
+    assert r0["counters"]["torn_reads"] == 0
+    for i, b1 in enumerate(r1["best"]):
+        if b1 < r0["pool_worst"][i] and b1 not in r0["pool_all"][i]:
+            assert b1 in r0["pool_after"][i] or min(r0["pool_after"][i]) < b1, i
+        assert r0["best"][i] <= min(b1, min(r0["pool_all"][i])), i
+    assert all(r0["valid"]) and all(r1["valid"])
+    assert r0["iters_ok"] and r1["iters_ok"]
