@@ -105,6 +105,9 @@ typedef struct RcpspSolveArgs {
                                  * initialised default) is always safe.  A
                                  * violated guarantee is caught on the device
                                  * (DE_SMEM) instead of corrupting memory. */
+    int32_t *ent_lock;          /* [I*F] per-entry locks (zeroed; ABI 8): the
+                                 * exchange locks one entry at a time, and
+                                 * ws_lock guards only the global best */
     /* live elite exchange between independent populations over peer memory
      * (ABI 8; all NULL / 0 = off).  Each population publishes its
      * per-instance global best in its outbox (seqlock: seq odd while being

@@ -142,6 +142,12 @@ __device__ __forceinline__ int stage_instance(const int* __restrict__ blob, int*
 
 __device__ __forceinline__ int align4(int words) { return (words + 3) & ~3; }
 
+// every demand of an activity sits in its record's demand word as an 8-bit
+// lane (one packing word of 8-bit lanes, so m <= 4)
+__device__ __forceinline__ bool cap_demand_packed(const SInst& I) {
+  return I.W == 1 && I.hi == 0x80808080u;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

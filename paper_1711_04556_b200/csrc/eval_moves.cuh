@@ -323,7 +323,8 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
                                                  int n, int m, int rs,
                                                  const uint32_t* __restrict__ moves,
                                                  int* __restrict__ cmax_out, int n_feas,
-                                                 int warp_words, bool reuse, uint32_t ctr_cl) {
+                                                 int warp_words, bool reuse, uint32_t ctr_cl,
+                                                 bool packed) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mr = m * rs;
   const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
@@ -374,7 +375,8 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
           f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
       const int esv = __reduce_max_sync(FULL_MASK, f);
       int req;
-      const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req);
+      const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req, packed,
+                                       static_cast<uint32_t>(rec.y));
       if (rec.x > 0) cap_update_all(a_c, rs, m, capk, req, start, rec.x);
       const int fin = start + rec.x;
       cm = max(cm, fin);
@@ -549,12 +551,12 @@ __device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, in
     eval_moves_cap_warp<true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
                               soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
                               c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
-                              n_feas, c.warp_words, reuse, ctr_cl);
+                              n_feas, c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I));
   else
     eval_moves_cap_warp<false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
                                soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
                                c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
-                               n_feas, c.warp_words, reuse, ctr_cl);
+                               n_feas, c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I));
 }
 
 // Cluster follower (rank > 0): evaluates moves of the leader's neighbourhood

@@ -554,6 +554,20 @@ __device__ __forceinline__ void add64(int64_t* p, long long v) {
   atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
+// ---- CTA-wide spin locks in global memory (thread 0 acquires, the CTA waits)
+__device__ __forceinline__ void cta_lock(int* lk) {
+  if (threadIdx.x == 0) {
+    while (atomicCAS(lk, 0, 1) != 0) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void cta_unlock(int* lk) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(lk, 0);
+}
+
 // ---- live elite exchange over peer memory (RcpspSolveArgs.outbox / peers)
 __device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
   int v;
@@ -591,13 +605,13 @@ __device__ void publish_best(const RcpspSolveArgs& A, int iid, const int* best, 
 // Import the best new foreign elite of instance iid, if it beats the pool's
 // worst entry and its makespan is not in the pool yet (k_merge_elites' rule):
 // the entry takes the order, its tabu list is cleared, IC and reads reset,
-// and the global best follows.  Warp 0 works (one peer per lane, n_peers <=
-// 32), the CTA waits; `stage` is free shared scratch of n words.  Caller
-// holds the instance lock.
+// and the global best follows.  Warp 0 reads the peers (one per lane,
+// n_peers <= 32) into `stage` (free shared scratch of n words); the writes
+// take the instance's best lock, then the entry's lock, like a write-back.
 template <int MODE>
-__device__ void import_peer_elite(const RcpspSolveArgs& A, int iid, int n, int* stage,
+__device__ void import_peer_elite(const RcpspSolveArgs& A, CtaCtx& c, int iid, int* stage,
                                   int64_t* Hd) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, n = c.I.n;
   const int np = static_cast<int>(A.n_peers), F = static_cast<int>(A.pool_size),
             T = static_cast<int>(A.tabu_size);
   const size_t W = RCPSP_OUTBOX_WORDS(A.n_max);
@@ -613,8 +627,10 @@ __device__ void import_peer_elite(const RcpspSolveArgs& A, int iid, int n, int* 
       if (seq != 0 && !(seq & 1) && seq != seen) key = (static_cast<unsigned>(cm) << 5) | lane;
     }
     const unsigned best = __reduce_min_sync(FULL_MASK, key);
+    int go = 0, ccm = 0, worst = 0;
     if (best != 0xffffffffu) {
-      const int src = static_cast<int>(best & 31u), ccm = static_cast<int>(best >> 5);
+      const int src = static_cast<int>(best & 31u);
+      ccm = static_cast<int>(best >> 5);
       const int sseq = __shfl_sync(FULL_MASK, seq, src);
       const int32_t* sob = reinterpret_cast<const int32_t*>(
           __shfl_sync(FULL_MASK, reinterpret_cast<unsigned long long>(pob), src));
@@ -629,48 +645,59 @@ __device__ void import_peer_elite(const RcpspSolveArgs& A, int iid, int n, int* 
       }
       dup = __any_sync(FULL_MASK, dup);
       wkey = __reduce_max_sync(FULL_MASK, wkey);
-      const int worst_c = static_cast<int>(wkey >> 16), worst = 0xffff - static_cast<int>(wkey & 0xffffu);
-      bool imported = false;
-      if (!dup && ccm < worst_c) {
+      worst = 0xffff - static_cast<int>(wkey & 0xffffu);
+      if (!dup && ccm < static_cast<int>(wkey >> 16)) {
         for (int p = lane; p < n; p += 32) stage[p] = ld_volatile_g(sob + 4 + p);
         __threadfence_system();
         __syncwarp();
         const int seq2 = __shfl_sync(FULL_MASK, lane == 0 ? ld_acquire_sys(sob) : 0, 0);
-        if (seq2 == sseq) {  // not overwritten meanwhile: a consistent order
-          const size_t eo = static_cast<size_t>(iid) * F + worst;
-          for (int p = lane; p < n; p += 32) A.ent_order[eo * A.n_max + p] = stage[p];
-          for (int i = lane; i < T; i += 32) A.ent_tabu[eo * T + i] = 0u;
-          const bool gb = ccm < ldcg64(&Hd[WS_BEST]);
-          if (gb)
-            for (int p = lane; p < n; p += 32)
-              A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] = stage[p];
-          if (lane == 0) {
-            A.ent_cmax[eo] = ccm;
-            A.ent_head[eo] = 0;
-            A.ent_ic[eo] = 0;
-            A.ent_reads[eo] = 0;
-            if (gb) {
-              Hd[WS_BEST] = ccm;
-              Hd[WS_BEST_MODE] = MODE;
-            }
-          }
-          imported = true;
-        } else if (lane == 0 && A.peer_stats) {
+        go = seq2 == sseq;  // not overwritten meanwhile: a consistent order
+        if (!go && lane == 0 && A.peer_stats)
           atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[3]), 1ull);
-        }
       }
-      // a consistent elite is consumed whether or not it entered the pool
-      if (lane == 0 && (imported || dup || ccm >= worst_c)) {
+      // a consistent elite is consumed whether or not it enters the pool
+      if (lane == 0 && (go || dup || ccm >= static_cast<int>(wkey >> 16)))
         A.peer_seen[static_cast<size_t>(iid) * np + src] = sseq;
-        if (imported && A.peer_stats)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[0]), 1ull);
-      }
     }
-    if (lane == 0 && A.peer_stats)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[2]), 1ull);
-    __syncwarp();
+    if (lane == 0) {
+      c.scal[SC_FLAG] = go;
+      c.scal[SC_PEERC] = ccm;
+      c.scal[SC_PEERW] = worst;
+      if (A.peer_stats) atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[2]), 1ull);
+    }
   }
   __syncthreads();
+  if (!c.scal[SC_FLAG]) return;
+  const int ccm = c.scal[SC_PEERC], worst = c.scal[SC_PEERW];
+  // the global best first (pool-min), then the entry
+  cta_lock(&A.ws_lock[iid]);
+  if (tid == 0) c.scal[SC_FLAG] = ccm < ldcg64(&Hd[WS_BEST]);
+  __syncthreads();
+  if (c.scal[SC_FLAG]) {
+    for (int p = tid; p < n; p += blockDim.x)
+      A.ws_best_order[static_cast<size_t>(iid) * A.n_max + p] = stage[p];
+    if (tid == 0) {
+      Hd[WS_BEST] = ccm;
+      Hd[WS_BEST_MODE] = MODE;
+    }
+  }
+  cta_unlock(&A.ws_lock[iid]);
+  const size_t eo = static_cast<size_t>(iid) * F + worst;
+  cta_lock(&A.ent_lock[eo]);
+  if (tid == 0) c.scal[SC_FLAG] = ccm < __ldcg(&A.ent_cmax[eo]);  // still worse than the elite?
+  __syncthreads();
+  if (c.scal[SC_FLAG]) {
+    for (int p = tid; p < n; p += blockDim.x) A.ent_order[eo * A.n_max + p] = stage[p];
+    for (int i = tid; i < T; i += blockDim.x) A.ent_tabu[eo * T + i] = 0u;
+    if (tid == 0) {
+      A.ent_cmax[eo] = ccm;
+      A.ent_head[eo] = 0;
+      A.ent_ic[eo] = 0;
+      A.ent_reads[eo] = 0;
+      if (A.peer_stats) atomicAdd(reinterpret_cast<unsigned long long*>(&A.peer_stats[0]), 1ull);
+    }
+  }
+  cta_unlock(&A.ent_lock[eo]);
 }
 
 // One CTA = one search worker.  Worker loop (search.run_worker): exchange
@@ -740,98 +767,127 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
   long long granted = 0, used = 0, polls = 0;
   int hops = 0;
   for (;;) {
-    // ---------------- exchange (cooperation.py:82-135), under the lock
-    if (tid == 0) {
-      while (atomicCAS(&A.ws_lock[iid], 0, 1) != 0) __nanosleep(100);
-      __threadfence();
-    }
-    __syncthreads();
+    // ---------------- exchange (cooperation.py:82-135), fine-grained: the
+    // instance lock ws_lock[iid] guards only the global best (taken by a
+    // worker that improves it), every pool entry has its own lock
+    // (ent_lock), the budget counters are atomics.  A single worker (B = 1)
+    // performs the reference's sequence of updates exactly; with B > 1 the
+    // workers of an instance no longer queue behind one another.
     if (entry >= 0) {
       const size_t eo = static_cast<size_t>(iid) * F + entry;
-      const long long gbest = ldcg64(&Hd[WS_BEST]);
-      if (improved) {
-        int* dst = A.ent_order + eo * A.n_max;
-        for (int p = tid; p < c.I.n; p += blockDim.x) dst[p] = c.best[p];
-        uint32_t* tl = A.ent_tabu + eo * T;
-        for (int i = tid; i < T; i += blockDim.x) tl[i] = c.tabu_list[i];
-        if (local_best < gbest) {
+      // 1. the global best first: it stays <= every pool entry (pool-min)
+      if (tid == 0) c.scal[SC_FLAG] = improved && local_best < ldcg64(&Hd[WS_BEST]);
+      __syncthreads();
+      if (c.scal[SC_FLAG]) {
+        cta_lock(&A.ws_lock[iid]);
+        if (tid == 0) c.scal[SC_FLAG] = local_best < ldcg64(&Hd[WS_BEST]);
+        __syncthreads();
+        if (c.scal[SC_FLAG]) {
           int* bo = A.ws_best_order + static_cast<size_t>(iid) * A.n_max;
           for (int p = tid; p < c.I.n; p += blockDim.x) bo[p] = c.best[p];
-        }
-      }
-      __syncthreads();
-      if (A.outbox && improved && local_best < gbest)
-        publish_best(A, iid, c.best, c.I.n, local_best);
-      if (tid == 0) {
-        const long long unused = granted - used;
-        Hd[WS_PLANNED] = ldcg64(&Hd[WS_PLANNED]) - (unused > 0 ? unused : 0);
-        Hd[WS_CONSUMED] = ldcg64(&Hd[WS_CONSUMED]) + used;
-        A.ent_ic[eo] = ldcg64(&A.ent_ic[eo]) + used;
-        if (improved) {
-          A.ent_cmax[eo] = local_best;
-          A.ent_head[eo] = c.scal[SC_HEAD];
-          A.ent_reads[eo] = 0;
-          if (local_best < gbest) {
+          if (A.outbox) publish_best(A, iid, c.best, c.I.n, local_best);
+          if (tid == 0) {
             Hd[WS_BEST] = local_best;
             Hd[WS_BEST_MODE] = MODE;
           }
         }
+        cta_unlock(&A.ws_lock[iid]);
+      }
+      // 2. the entry (write back an improvement) and the budget counters
+      if (improved) {
+        cta_lock(&A.ent_lock[eo]);
+        int* dst = A.ent_order + eo * A.n_max;
+        for (int p = tid; p < c.I.n; p += blockDim.x) dst[p] = c.best[p];
+        uint32_t* tl = A.ent_tabu + eo * T;
+        for (int i = tid; i < T; i += blockDim.x) tl[i] = c.tabu_list[i];
+        if (tid == 0) {
+          A.ent_cmax[eo] = local_best;
+          A.ent_head[eo] = c.scal[SC_HEAD];
+          A.ent_reads[eo] = 0;
+          A.ent_ic[eo] = ldcg64(&A.ent_ic[eo]) + used;
+        }
+        cta_unlock(&A.ent_lock[eo]);
+      } else if (tid == 0) {
+        add64(&A.ent_ic[eo], used);
+      }
+      if (tid == 0) {
+        const long long unused = granted - used;
+        if (unused > 0) add64(&Hd[WS_PLANNED], -unused);
+        add64(&Hd[WS_CONSUMED], used);
       }
       entry = -1;
       improved = 0;
       // the reference's pool-min invariant after every write-back
-      // (WorkingSet._assert_pool_min, cooperation.py:76-79, called by exchange)
+      // (WorkingSet._assert_pool_min, cooperation.py:76-79, called by exchange):
+      // entries read before the best, which only ever decreases
       __syncthreads();
       bool above = false;
-      for (int i = tid; i < F; i += blockDim.x)
-        above |= static_cast<long long>(__ldcg(&A.ent_cmax[static_cast<size_t>(iid) * F + i])) <
-                 ldcg64(&Hd[WS_BEST]);
+      for (int i = tid; i < F; i += blockDim.x) {
+        const long long v = __ldcg(&A.ent_cmax[static_cast<size_t>(iid) * F + i]);
+        __threadfence();
+        above |= v < ldcg64(&Hd[WS_BEST]);
+      }
       if (__syncthreads_or(above) && tid == 0) set_err(A.err, DE_POOL_MIN);
     }
     // live elite exchange: poll the other populations' outboxes (c.best is
     // free here: the write-back above has consumed it)
     if (A.n_peers > 0 && ++polls % A.poll_every == 0)
-      import_peer_elite<MODE>(A, iid, c.I.n, c.best, Hd);
+      import_peer_elite<MODE>(A, c, iid, c.best, Hd);
+    // ---------------- stop test, then the next entry round robin
     if (tid == 0) {
       const long long best = ldcg64(&Hd[WS_BEST]);
       if (best <= ldcg64(&Hd[WS_FLOOR])) Hd[WS_STOP] = 1;
       if (budget_spent(c.budget_ns, c.t0_ns)) Hd[WS_STOP] = 1;
-      const long long planned = ldcg64(&Hd[WS_PLANNED]);
-      if (ldcg64(&Hd[WS_STOP]) || planned >= A.epoch_limit) {
-        c.scal[SC_NONE] = 1;
-      } else {
-        c.scal[SC_NONE] = 0;
-        const long long cursor = ldcg64(&Hd[WS_CURSOR]);
-        const int index = static_cast<int>(cursor % F);
-        Hd[WS_CURSOR] = cursor + 1;
-        const size_t eo = static_cast<size_t>(iid) * F + index;
+      const bool none = ldcg64(&Hd[WS_STOP]) || ldcg64(&Hd[WS_PLANNED]) >= A.epoch_limit;
+      c.scal[SC_NONE] = none ? 1 : 0;
+      c.scal[SC_BESTK] = static_cast<int>(best);
+      if (!none)
+        c.scal[SC_ENTRY] = static_cast<int>(
+            atomicAdd(reinterpret_cast<unsigned long long*>(&Hd[WS_CURSOR]), 1ull) %
+            static_cast<unsigned long long>(F));
+    }
+    __syncthreads();
+    if (!c.scal[SC_NONE]) {
+      // adopt the entry under its lock: order, tabu list, Eq. 8 grant
+      const size_t eo = static_cast<size_t>(iid) * F + c.scal[SC_ENTRY];
+      cta_lock(&A.ent_lock[eo]);
+      const int* src = A.ent_order + eo * A.n_max;
+      for (int p = tid; p < c.I.n; p += blockDim.x) c.base[p] = __ldcg(&src[p]);
+      const uint32_t* tl = A.ent_tabu + eo * T;
+      for (int i = tid; i < T; i += blockDim.x) c.tabu_list[i] = __ldcg(&tl[i]);
+      if (tid == 0) {
         const long long reads = ldcg64(&A.ent_reads[eo]) + 1;
         A.ent_reads[eo] = reads;
         const int ecm = __ldcg(&A.ent_cmax[eo]);
-        long long grant = eq8(ecm, ldcg64(&A.ent_ic[eo]), A.block_iters, best);
+        long long grant = eq8(ecm, ldcg64(&A.ent_ic[eo]), A.block_iters, c.scal[SC_BESTK]);
         if (grant < 1) grant = 1;
         if (A.grant_cap > 0 && grant > A.grant_cap) grant = A.grant_cap;
-        const long long room = A.total_iters - planned;
-        const long long eroom = A.epoch_limit - planned;
-        if (grant > room) grant = room;
-        if (grant > eroom) grant = eroom;
-        Hd[WS_PLANNED] = planned + grant;
-        c.scal[SC_ENTRY] = index;
-        c.scal[SC_GRANT] = static_cast<int>(grant);
+        // claim the grant from the budget (another worker may have moved it)
+        long long p = ldcg64(&Hd[WS_PLANNED]), g = 0;
+        for (;;) {
+          if (p >= A.epoch_limit) {
+            g = 0;
+            break;
+          }
+          g = grant;
+          if (g > A.total_iters - p) g = A.total_iters - p;
+          if (g > A.epoch_limit - p) g = A.epoch_limit - p;
+          const long long q = static_cast<long long>(atomicCAS(
+              reinterpret_cast<unsigned long long*>(&Hd[WS_PLANNED]),
+              static_cast<unsigned long long>(p), static_cast<unsigned long long>(p + g)));
+          if (q == p) break;
+          p = q;
+        }
+        c.scal[SC_GRANT] = static_cast<int>(g);
         c.scal[SC_ADOPT] = ecm;
-        c.scal[SC_BESTK] = static_cast<int>(best);
         c.scal[SC_DIV] = reads > A.phi_max ? 1 : 0;
         c.scal[SC_HEAD] = __ldcg(&A.ent_head[eo]) % T;
+        if (g == 0) c.scal[SC_NONE] = 1;  // the budget ran out meanwhile (B > 1)
       }
+      cta_unlock(&A.ent_lock[eo]);
     }
-    __syncthreads();
     if (c.scal[SC_NONE]) {
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        atomicExch(&A.ws_lock[iid], 0);
-        atomicMax(reinterpret_cast<unsigned long long*>(&Hd[WS_T1]), globaltimer());
-      }
+      if (tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(&Hd[WS_T1]), globaltimer());
       if (!steal) break;
       // ---------------- move on to an instance that still has budget
       if (tid == 0) {
@@ -865,16 +921,6 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
     const int adopted = c.scal[SC_ADOPT];
     const int best_known = c.scal[SC_BESTK];
     const bool needs_div = c.scal[SC_DIV] != 0;
-    {
-      const size_t eo = static_cast<size_t>(iid) * F + entry;
-      const int* src = A.ent_order + eo * A.n_max;
-      for (int p = tid; p < c.I.n; p += blockDim.x) c.base[p] = __ldcg(&src[p]);
-      const uint32_t* tl = A.ent_tabu + eo * T;
-      for (int i = tid; i < T; i += blockDim.x) c.tabu_list[i] = __ldcg(&tl[i]);
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) atomicExch(&A.ws_lock[iid], 0);
     cta_tabu_rebuild(c);
     // ---------------- run_worker body (search.py:189-194)
     if (needs_div) cta_diversify(c, c.base, static_cast<int>(A.phi_steps), rng);
@@ -1272,6 +1318,7 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
   if (threads % 32 || threads < 0 || threads > KSOLVE_THREADS_MAX)
     return fail("threads must be 0 (auto) or 32.." + std::to_string(KSOLVE_THREADS_MAX) + ", x32");
   if (A.tabu_size < 1) return fail("tabu_size must be >= 1");
+  if (A.ent_lock == nullptr) return fail("RcpspSolveArgs.ent_lock is required (ABI 8)");
   if (A.n_peers < 0 || A.n_peers > 32) return fail("n_peers must be 0..32");
   if (A.n_peers > 0 && (A.peers == nullptr || A.peer_seen == nullptr || A.poll_every < 1))
     return fail("peer exchange needs peers, peer_seen and poll_every >= 1");

@@ -687,6 +687,96 @@ __device__ __forceinline__ void cap_update_warp(uint32_t a_row, int capk, int r,
   __syncwarp();
 }
 
+// cap_update_warp for rows of up to 32*K entries and demands r < 32: the row
+// is read once into K registers per lane (entry 32k + lane in v[k]); the
+// shifted value c[i - r] comes from the lane r to the left (one chunk back
+// for lanes < r), the scan and the writes run on registers -- one LDS and one
+// STS per entry instead of the generic path's re-reads.
+template <int K>
+__device__ __forceinline__ void cap_update_reg(uint32_t a_row, int capk, int r, int s, int d) {
+  const int lane = threadIdx.x & 31;
+  const int T = s + d;
+  int v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = 32 * k + lane;
+    v[k] = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+  }
+  int i0 = capk, c0 = 0;
+#pragma unroll
+  for (int k = K - 1; k >= 0; --k) {  // the lowest chunk holding an entry < T decides
+    const unsigned msk = __ballot_sync(FULL_MASK, 32 * k + lane < capk && v[k] < T);
+    if (msk) {
+      const int l = __ffs(msk) - 1;
+      i0 = 32 * k + l;
+      c0 = __shfl_sync(FULL_MASK, v[k], l);
+    }
+  }
+  if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
+  if (c0 <= s) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = 32 * k + lane;
+      if (i >= i0 && i < i0 + r) sts32(a_row + 4 * i, static_cast<uint32_t>(T));
+    }
+    __syncwarp();
+    return;
+  }
+  int oir[K];
+  int carry = 0, t = capk, newt = 0;
+  bool done = false;
+  const int srcl = (lane - r) & 31;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = 32 * k + lane;
+    const int a = __shfl_sync(FULL_MASK, v[k], srcl);
+    const int b = k > 0 ? __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], srcl) : 0;
+    oir[k] = lane >= r ? a : b;  // c[i - r]
+    if (!done) {
+      const bool in = i < capk, sh = i >= i0 + r;
+      const int f = max(v[k], s);
+      const int g = (in && i >= i0) ? (sh ? oir[k] - f : s - f) : 0;
+      int S = g;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, S, o);
+        if (lane >= o) S += y;
+      }
+      S += carry;
+      const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
+      if (term) {
+        const int l = __ffs(term) - 1;
+        t = 32 * k + l;
+        newt = __shfl_sync(FULL_MASK, f - (S - g), l);
+        done = true;
+      } else {
+        carry = __shfl_sync(FULL_MASK, S, 31);
+      }
+    }
+  }
+  const int end = t < capk ? t : capk;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = 32 * k + lane;
+    if (i >= i0 && i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : oir[k]));
+    if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+  }
+  __syncwarp();
+}
+
+// Alg. 4 on one row: the register-resident form for rows up to 96 entries
+// and demands below 32, else the generic one.
+__device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
+  if (r < 32 && capk <= 32)
+    cap_update_reg<1>(a_row, capk, r, s, d);
+  else if (r < 32 && capk <= 64)
+    cap_update_reg<2>(a_row, capk, r, s, d);
+  else if (r < 32 && capk <= 96)
+    cap_update_reg<3>(a_row, capk, r, s, d);
+  else
+    cap_update_warp(a_row, capk, r, s, d);
+}
+
 // Alg. 4 for every resource the activity demands (lane k < m: capacity and
 // demand of resource k), one after another with the whole warp.
 __device__ __forceinline__ void cap_update_all(uint32_t a_c, int rs, int m, int capk, int req,
@@ -696,21 +786,25 @@ __device__ __forceinline__ void cap_update_all(uint32_t a_c, int rs, int m, int 
   while (used) {
     const int k = __ffs(used) - 1;
     used &= used - 1;
-    cap_update_warp(a_c + 4 * k * rs, __shfl_sync(FULL_MASK, capk, k),
-                    __shfl_sync(FULL_MASK, req, k), start, dur);
+    cap_update_row(a_c + 4 * k * rs, __shfl_sync(FULL_MASK, capk, k),
+                   __shfl_sync(FULL_MASK, req, k), start, dur);
   }
 }
 
 // Eq. 7 start (kernels.py:68-78, also for zero durations, as kernels.py:
 // 182-186) of an activity whose precedence bound is esv; req: lane k < m gets
 // resource k's demand.
+// packed: the record's demand word holds every demand as an 8-bit lane (one
+// packing word, 8-bit lanes: m <= 4), so no demand load is needed.
 __device__ __forceinline__ int cap_start_warp(int act, int esv, uint32_t a_dem, int m, int capk,
-                                              int rs, uint32_t a_c, int& req) {
+                                              int rs, uint32_t a_c, int& req,
+                                              bool packed = false, uint32_t dword = 0u) {
   const int lane = threadIdx.x & 31;
   int t = 0;
   req = 0;
   if (lane < m) {
-    req = static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
+    req = packed ? static_cast<int>((dword >> (8 * lane)) & 0xffu)
+                 : static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
     if (req > 0) t = static_cast<int>(lds32(a_c + 4 * (lane * rs + capk - req)));
   }
   return max(esv, __reduce_max_sync(FULL_MASK, t));

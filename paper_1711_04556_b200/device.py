@@ -509,6 +509,7 @@ class BatchSolver:
         self.d_blob = z(len(self.blob_cat), i32)
         self.d_offs = z(I, i64)
         self.ws_lock = z(I, i32)
+        self.ent_lock = z((I, F), i32)
         self.ws_hdr = z((I, 16), i64)
         self.ent_order = z((I, F, n_max), i32)
         self.ent_cmax = z((I, F), i32)
@@ -552,7 +553,7 @@ class BatchSolver:
 
     def reset(self) -> None:
         """Zero the working set and worker state (re-running the same batch)."""
-        for t in (self.ws_lock, self.ws_hdr, self.ent_order, self.ent_cmax, self.ent_tabu,
+        for t in (self.ws_lock, self.ent_lock, self.ws_hdr, self.ent_order, self.ent_cmax, self.ent_tabu,
                   self.ent_head, self.ent_ic, self.ent_reads, self.best_order, self.w_stats,
                   self.err):
             t.zero_()
@@ -575,6 +576,7 @@ class BatchSolver:
         a.epoch_limit = cfg.total_iters if epoch_limit is None else epoch_limit
         a.grant_cap, a.collect_trace = cfg.grant_cap, int(cfg.collect_trace)
         a.ws_lock, a.ws_hdr = ptr(self.ws_lock), ptr(self.ws_hdr)
+        a.ent_lock = ptr(self.ent_lock)
         a.ent_order, a.ent_cmax, a.ent_tabu = ptr(self.ent_order), ptr(self.ent_cmax), ptr(self.ent_tabu)
         a.ent_head, a.ent_ic, a.ent_reads = ptr(self.ent_head), ptr(self.ent_ic), ptr(self.ent_reads)
         a.ws_best_order = ptr(self.best_order)

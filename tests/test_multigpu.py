@@ -145,7 +145,7 @@ def _gpu_worker(rank: int, world: int, port: int, kind: str, out):
         r = s.collect()
         res["rounds"] = ex.rounds
     else:
-        iters = 300 if rank == 1 else 5
+        iters = 2000 if rank == 1 else 5
         cfg = SolveConfig(total_iters=iters, workers=1, pool_size=8, tabu_size=250, delta=60,
                           phi_steps=20, phi_max=3, seed=1000 * rank)
         s = BatchSolver(insts, [1] * 6, cfg)
@@ -206,7 +206,9 @@ def test_two_rank_peer_exchange():
     imports every foreign elite that beats its pool's worst entry; imported
     orders are consistent (their evaluation equals the claimed makespan)."""
     r0, r1 = _spawn_gpu("peer")
-    assert r1["counters"]["publishes"] > 0
+    improved = sum(b < min(p) for b, p in zip(r1["best"], r1["pool_all"]))
+    # every improvement of a global best is published (at least once)
+    assert r1["counters"]["publishes"] >= improved > 0, (r1["counters"], improved)
     assert r0["counters"]["polls"] > 0 and r0["counters"]["imports"] > 0
     assert r0["counters"]["torn_reads"] == 0
     for i, b1 in enumerate(r1["best"]):
