@@ -105,6 +105,10 @@ typedef struct RcpspSolveArgs {
                                  * initialised default) is always safe.  A
                                  * violated guarantee is caught on the device
                                  * (DE_SMEM) instead of corrupting memory. */
+    int64_t sumcap_max;         /* max over the instances of the sum of the
+                                 * capacities (RcpspShape.sumcap): sizes the
+                                 * CAPACITY evaluator's state snapshots (0 =
+                                 * no snapshots, no convergence exit) */
     int32_t *ent_lock;          /* [I*F] per-entry locks (zeroed; ABI 8): the
                                  * exchange locks one entry at a time, and
                                  * ws_lock guards only the global best */
@@ -139,6 +143,7 @@ typedef struct RcpspShape {
     int32_t cpm;        /* critical-path length (the search's floor)         */
     int32_t len;        /* blob length in int32 words                        */
     int32_t big;        /* a duration or fan-out/-in above 32                */
+    int32_t sumcap;     /* sum of the capacities (CAPACITY state words)      */
 } RcpspShape;
 
 int rcpsp_abi_version(void);

@@ -29,6 +29,8 @@ struct CtaCtx {
   int* red;        // [72] reduction scratch
   int* scal;       // [SC_WORDS]
   int* evs;        // evaluation scratch (per warp)
+  int* snap;       // CAPACITY: uint16 [n][S] state after every position of the
+                   // current schedule (convergence exit), or null
   int warp_words;  // evaluation scratch words per warp
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
   bool inc;        // TIME G = 32: reuse the current order's schedule prefix

@@ -305,35 +305,47 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req,
 
 // CAP, one warp per schedule, reusing the current order's schedule prefix
 // like eval_moves_time32_inc.  Alg. 4 runs in closed form with the whole warp
-// (sgs.cuh: cap_update_warp).  Its state depends on the update order, not
-// only on the set of starts, so there is no undo and no convergence exit:
-// each move copies the prefix state c_pre and schedules positions u..n-1.
-// Precedence is pulled as in the TIME evaluator: es = max over the
-// predecessors' finish times fin[] (the prefix activities hold the current
-// schedule's, the suffix overwrites its own before a successor reads them),
-// so no per-move es copy.  With reuse == false the prefix stays empty (full
-// SGS of every swapped order).  The zero-duration sink is not scheduled (its
-// start, max(es, Eq. 7), is bounded by the finish times already in the
+// (sgs.cuh: cap_update_row); the state is compact (row k at the sum of the
+// capacities before it, S words).  Precedence is pulled as in the TIME
+// evaluator: es = max over the predecessors' finish times fin[] (the prefix
+// activities hold the current schedule's, the suffix overwrites its own
+// before a successor reads them).  The zero-duration sink is not scheduled
+// (its start, max(es, Eq. 7), is bounded by the finish times already in the
 // makespan).
-//   per-warp scratch: c [m*rs] | c_pre [m*rs] | fin [n]
+//
+// SNAP: the current schedule's state after every position is in shared
+// memory (uint16 [n][S], written by the base pass, o_snap).  A move then
+// starts from the snapshot at u-1 (no prefix state to extend), and if every
+// activity at positions u..v starts where it does in the current schedule
+// AND the state after v equals the snapshot at v, the rest of the schedule is
+// the current one: C_max = base_cmax (convergence exit).  Capacity-indexed
+// states depend on the order of the updates, so the state is compared, not
+// implied by the starts as in TIME.
+// !SNAP (large n*S): each warp extends a prefix state c_pre with the known
+// starts as u grows and copies it per move; no convergence exit.
+//   per-warp scratch: c [S] | c_pre [S] (!SNAP) | fin [n]; S <= m*rs
 //   o_info: pull records (info_r); o_pull: padded predecessor lists (pdat)
-template <bool BIG>
+template <bool BIG, bool SNAP>
 __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_dem, int o_cap,
                                                  int o_base, int o_bst, int o_ctr, int o_evs,
-                                                 int n, int m, int rs,
+                                                 int o_snap, int n, int m, int rs,
                                                  const uint32_t* __restrict__ moves,
                                                  int* __restrict__ cmax_out, int n_feas,
                                                  int warp_words, bool reuse, uint32_t ctr_cl,
-                                                 bool packed) {
+                                                 bool packed, int base_cmax) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mr = m * rs;
-  const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
-  const uint32_t a_c = a_scr, a_cp = a_c + 4 * mr, a_fin = a_cp + 4 * mr;
-  const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
-                 a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr);
-  const uint32_t a_pdat_l = opaque(a_pdat + 4 * lane);
   const int capk = lane < m ? dsm[o_cap + lane] : 0;
-  for (int j = lane; j < mr; j += 32) sts32(a_cp + 4 * j, 0);
+  const int off = cap_row_offset(capk);
+  const int S = __shfl_sync(FULL_MASK, off + capk, 31);
+  const int mr = m * rs;  // >= S: the scratch layout's row budget
+  const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
+  const uint32_t a_c = a_scr, a_cp = a_c + 4 * mr, a_fin = a_cp + (SNAP ? 0u : 4u * mr);
+  const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
+                 a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
+                 a_snap = SNAP ? sa(dsm + o_snap) : 0u;
+  const uint32_t a_pdat_l = opaque(a_pdat + 4 * lane);
+  if (!SNAP)
+    for (int j = lane; j < S; j += 32) sts32(a_cp + 4 * j, 0);
   __syncwarp();
   const int pend = lds128(a_info + 16 * static_cast<int>(lds32(a_base + 4 * (n - 1)))).x == 0
                        ? n - 1 : n;
@@ -346,24 +358,35 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
     const uint32_t mv = moves[idx];
     const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
     const int u0 = reuse ? u : 0;
-    // ---- extend the prefix state to positions < u0 with the known starts
+    // ---- positions < u0: the current schedule's finish times (and, !SNAP,
+    // its state extended with the known starts)
     for (; up < u0; ++up) {
       const int act = static_cast<int>(lds32(a_base + 4 * up));
-      const int dur = lds128(a_info + 16 * act).x;
+      const int4 rec = lds128(a_info + 16 * act);
       const int st = static_cast<int>(lds32(a_bst + 4 * act));
-      if (dur > 0) {
-        const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
-        cap_update_all(a_cp, rs, m, capk, req, st, dur);
+      if (!SNAP && rec.x > 0) {
+        int req = 0;
+        if (lane < m)
+          req = packed ? static_cast<int>((static_cast<uint32_t>(rec.y) >> (8 * lane)) & 0xffu)
+                       : static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
+        cap_update_all(a_cp, off, m, capk, req, st, rec.x);
       }
-      cm_pre = max(cm_pre, st + dur);
-      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(st + dur));
+      cm_pre = max(cm_pre, st + rec.x);
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(st + rec.x));
       __syncwarp();
     }
-    for (int j = lane; j < mr; j += 32) sts32(a_c + 4 * j, lds32(a_cp + 4 * j));
+    if (SNAP && u0 > 0) {
+      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, lds16(a_snap + 2 * ((u0 - 1) * S + j)));
+    } else if (SNAP) {
+      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, 0);
+    } else {
+      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, lds32(a_cp + 4 * j));
+    }
     __syncwarp();
     // ---- positions u0.. of the swapped order
-    int cm = cm_pre;
-    for (int p = u0; p < pend; ++p) {
+    int cm = cm_pre, p = u0;
+    bool div = !SNAP || !reuse;
+    for (; p < pend; ++p) {
       const int q = p == u ? v : (p == v ? u : p);
       const int act = static_cast<int>(lds32(a_base + 4 * q));
       const int4 rec = lds128(a_info + 16 * act);
@@ -375,16 +398,30 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
           f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
       const int esv = __reduce_max_sync(FULL_MASK, f);
       int req;
-      const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req, packed,
+      const int start = cap_start_warp(act, esv, a_dem, m, capk, off, a_c, req, packed,
                                        static_cast<uint32_t>(rec.y));
-      if (rec.x > 0) cap_update_all(a_c, rs, m, capk, req, start, rec.x);
+      if (rec.x > 0) cap_update_all(a_c, off, m, capk, req, start, rec.x);
       const int fin = start + rec.x;
       cm = max(cm, fin);
       sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
+      if (SNAP && !div) {
+        div = start != static_cast<int>(lds32(a_bst + 4 * act));
+        if (!div && p == v) {  // same starts through v: compare the state
+          __syncwarp();
+          bool diff = false;
+          for (int j = lane; j < S; j += 32)
+            diff |= lds32(a_c + 4 * j) != lds16(a_snap + 2 * (v * S + j));
+          if (!__any_sync(FULL_MASK, diff)) {
+            ++p;
+            break;  // converged: the rest is the current schedule
+          }
+          div = true;
+        }
+      }
       __syncwarp();
     }
-    if (lane == 0) cmax_out[idx] = cm;
-    steps += pend - u0;
+    if (lane == 0) cmax_out[idx] = (SNAP && !div) ? base_cmax : cm;
+    steps += p - u0;
   }
   if (lane == 0) {
     if (ctr_cl)
@@ -465,7 +502,7 @@ __device__ __noinline__ void eval_moves_cap_thread_inc(const SInst& I, int o_bas
       const int dur = I.dur[act], s0 = bst[act];
       if (dur > 0) {
         const int req = lane < m ? static_cast<int>(lds32(a_dem + 4 * (act * m + lane))) : 0;
-        cap_update_all(a_cpre, rs, m, capk, req, s0, dur);
+        cap_update_all(a_cpre, lane * rs, m, capk, req, s0, dur);
       }
       const int fin = s0 + dur;
       cm_pre = max(cm_pre, fin);
@@ -545,18 +582,30 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
 }
 
 // the prefix-reusing CAPACITY warp evaluator on this CTA's copy of the current order
-__device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
-                                                             bool reuse, uint32_t ctr_cl) {
-  if (c.I.big)
-    eval_moves_cap_warp<true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
-                              soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
-                              c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
-                              n_feas, c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I));
+template <bool BIG>
+__device__ __forceinline__ void eval_moves_cap_warp_snap(const CtaCtx& c, int n_feas, bool reuse,
+                                                         uint32_t ctr_cl, int base_cmax) {
+  if (c.snap)
+    eval_moves_cap_warp<BIG, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem),
+                                   soff(c.I.cap), soff(c.base), soff(c.bst),
+                                   soff(c.scal + SC_CTR), soff(c.evs), soff(c.snap), c.I.n, c.I.m,
+                                   cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
+                                   c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I), base_cmax);
   else
-    eval_moves_cap_warp<false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
-                               soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
-                               c.I.n, c.I.m, cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf,
-                               n_feas, c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I));
+    eval_moves_cap_warp<BIG, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem),
+                                    soff(c.I.cap), soff(c.base), soff(c.bst),
+                                    soff(c.scal + SC_CTR), soff(c.evs), 0, c.I.n, c.I.m,
+                                    cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
+                                    c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I),
+                                    base_cmax);
+}
+__device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
+                                                             bool reuse, uint32_t ctr_cl,
+                                                             int base_cmax) {
+  if (c.I.big)
+    eval_moves_cap_warp_snap<true>(c, n_feas, reuse, ctr_cl, base_cmax);
+  else
+    eval_moves_cap_warp_snap<false>(c, n_feas, reuse, ctr_cl, base_cmax);
 }
 
 // Cluster follower (rank > 0): evaluates moves of the leader's neighbourhood
@@ -586,12 +635,19 @@ __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, 
       c.base[p] = static_cast<int>(ld_cluster(l_base + 4 * p));
       c.bst[p] = static_cast<int>(ld_cluster(l_bst + 4 * p));
     }
+    if (MODE == MODE_CAPACITY && c.snap) {  // the current schedule's state snapshots
+      int S = 0;
+      for (int k = 0; k < c.I.m; ++k) S += c.I.cap[k];
+      const uint32_t l_snap = cluster_map(sa(c.snap), 0);
+      for (int w = tid; w < (c.I.n * S + 1) / 2; w += blockDim.x)
+        c.snap[w] = static_cast<int>(ld_cluster(l_snap + 4 * w));
+    }
     __syncthreads();
     const uint32_t ctr = l_scal + 4 * SC_CTR;
     if constexpr (MODE == MODE_TIME) {
       eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, ctr);
     } else if constexpr (G == 32) {
-      eval_moves_cap_warp_dispatch(c, n_feas, true, ctr);
+      eval_moves_cap_warp_dispatch(c, n_feas, true, ctr, base_cmax);
     } else {
       eval_moves_cap_thread_inc(c.I, soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
                                 soff(c.evs), c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
@@ -646,17 +702,20 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
     // the current order's schedule (starts -> bst), then one warp per move
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {
+      int cm = 0;
       if (c.inc)
-        sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
-                     cap_row_stride(c.I.rmax), sa(c.evs), sa(c.base), c.bst);
+        cm = sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
+                          cap_row_stride(c.I.rmax), sa(c.evs), sa(c.base), c.bst,
+                          c.snap ? sa(c.snap) : 0u);
       if (lane == 0) {
         c.scal[SC_CTR] = 0;
         c.scal[SC_STEPS] = c.inc ? c.I.n : 0;
+        c.scal[SC_BASEC] = cm;
       }
     }
     __syncthreads();
     cluster_phase_begin(c, n_feas);
-    eval_moves_cap_warp_dispatch(c, n_feas, c.inc, cluster_counter(c));
+    eval_moves_cap_warp_dispatch(c, n_feas, c.inc, cluster_counter(c), c.scal[SC_BASEC]);
     cluster_phase_end(c);
   } else {
     // prefix reuse pays from j60 on; on j30-size projects the per-batch state

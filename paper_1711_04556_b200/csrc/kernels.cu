@@ -58,7 +58,7 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
                                          int* err) {
   const bool ok = blob[B_MAGIC] == BLOB_MAGIC && blob[B_N] == s.n && blob[B_M] == s.m &&
                   blob[B_H] == s.horizon && blob[B_E] == s.edges && blob[B_W] == s.words &&
-                  blob[B_RMAX] == s.rmax;
+                  blob[B_RMAX] == s.rmax && blob[B_SUMCAP] == s.sumcap;
   if (!ok && threadIdx.x == 0) set_err(err, DE_BAD_BLOB);
   return ok;
 }
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, R
     for (int j = lane; j < m * R; j += 32) st[j] = state[j];
     __syncwarp();
     const int capk = lane < m ? I.cap[lane] : 0, req = lane < m ? dem[lane] : 0;
-    if (dur > 0) cap_update_all(sa(st), R, m, capk, req, arg, dur);
+    if (dur > 0) cap_update_all(sa(st), lane * R, m, capk, req, arg, dur);
     __syncwarp();
     for (int j = lane; j < m * R; j += 32) state[j] = st[j];
     if (lane == 0) out[0] = 0;
@@ -1046,6 +1046,7 @@ int shape_hdr(const RcpspShape* s, Hdr& h) {
     return fail("RcpspShape out of range (use rcpsp_blob_shape on the packed blob)");
   h.n = s->n; h.m = s->m; h.H = s->horizon; h.e = s->edges; h.W = s->words; h.lb = s->lane_bits;
   h.rmax = s->rmax; h.cpm = s->cpm;
+  if (s->sumcap < 0 || s->sumcap > s->m * s->rmax) return fail("RcpspShape.sumcap out of range");
   return 0;
 }
 
@@ -1073,10 +1074,10 @@ size_t smem_per_sm() {
 // memory fits `limit` bytes
 bool fit_plan_limit(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
                     int T, int want_threads, size_t limit, int min_threads, SmemPlan& p,
-                    int& threads, int big = 1) {
+                    int& threads, int big = 1, int sumcap = 0) {
   for (threads = want_threads; threads >= min_threads; threads -= 32) {
     for (int lanes = 32; lanes >= (mode == MODE_CAPACITY && G == 1 ? 1 : 32); --lanes) {
-      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes, big);
+      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes, big, sumcap);
       if (static_cast<size_t>(p.total) * 4 <= limit) return true;
     }
   }
@@ -1102,26 +1103,27 @@ int sm_count() {
 // threads per SM, j60: 354 M vs 311 M; j120: 2 x 512 stays best)
 bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
                      int T, int want_threads, SmemPlan& p, int& threads, long long grid = 0,
-                     int big = 1) {
+                     int big = 1, int sumcap = 0) {
   if (want_threads == 0 && n <= 64 && grid > 0) {
     const long long sms = sm_count();
     for (int per_sm : {8, 4}) {
       if (grid < per_sm * sms) continue;
       const int nt = 1024 / per_sm;
       const size_t lim = smem_per_sm() / per_sm - 1024;
-      if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, nt, lim, nt, p, threads, big))
+      if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, nt, lim, nt, p, threads, big,
+                         sumcap))
         return true;
     }
   }
   if (want_threads == 0) {
     const size_t half = smem_per_sm() / 2 - 1024;
     if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, ksolve_threads(mode, G), half,
-                       256, p, threads, big))
+                       256, p, threads, big, sumcap))
       return true;
     want_threads = 512;
   }
   return fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, want_threads, smem_optin(), 32, p,
-                        threads, big);
+                        threads, big, sumcap);
 }
 
 template <class Kern>
@@ -1238,7 +1240,8 @@ int rcpsp_run_chunk_batch(const int32_t* blob, const RcpspShape* shape, int mode
   return dispatch(mode, group, h.W, h.m, [&]<int MODE, int G, int W>() -> int {
     SmemPlan p;
     int nt;
-    if (!fit_search_plan(MODE, G, h.W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads, p, nt))
+    if (!fit_search_plan(MODE, G, h.W, h.n, h.m, h.H, h.e, h.rmax, delta, tabu_size, threads, p, nt,
+                         0, 1, shape->sumcap))
       return fail("search state does not fit in shared memory");
     auto k = k_run_chunk<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;
@@ -1334,7 +1337,8 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.h_max), static_cast<int>(A.e_max),
                          static_cast<int>(A.rmax_max), static_cast<int>(A.delta),
                          static_cast<int>(A.tabu_size), threads, p, nt,
-                         static_cast<long long>(n_ids) * A.workers, A.no_big ? 0 : 1))
+                         static_cast<long long>(n_ids) * A.workers, A.no_big ? 0 : 1,
+                         static_cast<int>(A.sumcap_max)))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
     if (set_smem(k, p.total * 4)) return -1;

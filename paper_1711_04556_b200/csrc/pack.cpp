@@ -13,8 +13,9 @@
 // CAPACITY mode only), the critical-path length (instance.py:374-388, the
 // sink's longest duration-weighted distance), the precedence levels
 // (instance.py:396-415: longest unit-weight distance from any root, ids
-// ascending inside a level) and the B_BIG flag (a duration, fan-out or --
-// except into a zero-duration sink -- fan-in above 32).
+// ascending inside a level), the B_BIG flag (a duration, fan-out or --
+// except into a zero-duration sink -- fan-in above 32) and B_SUMCAP (the sum
+// of the capacities: the compact capacity-indexed state's size).
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -30,7 +31,7 @@ constexpr int kKeyLimit = 1 << 16;   // selection key packs (C_max << 16) | rank
 
 enum {
   B_MAGIC = 0, B_N = 1, B_M = 2, B_H = 3, B_E = 4, B_W = 5, B_LB = 6, B_RMAX = 7, B_CPM = 8,
-  B_LEN = 9, B_NLVL = 10, B_BIG = 11,
+  B_LEN = 9, B_NLVL = 10, B_BIG = 11, B_SUMCAP = 12,
   B_OFF_DUR = 16, B_OFF_DEM, B_OFF_CAP, B_OFF_PPTR, B_OFF_PDAT, B_OFF_SPTR, B_OFF_SDAT,
   B_OFF_REQ, B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT
 };
@@ -212,6 +213,9 @@ int rcpsp_pack_instance(const int32_t* dur, const int32_t* dem, const int32_t* c
   blob[B_LEN] = static_cast<int32_t>(off);
   blob[B_NLVL] = d.n_levels;
   blob[B_BIG] = d.big;
+  int sumcap = 0;
+  for (int k = 0; k < m; ++k) sumcap += cap[k];
+  blob[B_SUMCAP] = sumcap;
   return 0;
 }
 
@@ -228,6 +232,7 @@ int rcpsp_blob_shape(const int32_t* blob, RcpspShape* shape) {
   shape->cpm = blob[B_CPM];
   shape->len = blob[B_LEN];
   shape->big = blob[B_BIG];
+  shape->sumcap = blob[B_SUMCAP];
   return 0;
 }
 

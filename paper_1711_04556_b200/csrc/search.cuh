@@ -143,21 +143,27 @@ __device__ void cta_diversify(CtaCtx& c, int* work, int steps, Pcg64& rng) {
 struct SmemPlan {
   int inst, base, pos, msp, mpp, rs, best, rowc, bst, tabu_list, tabu_cnt, red, scal, evs;
   int warp_words, total, cap_lanes;
+  int snap;  // CAPACITY group 32: state snapshots (uint16 [n][S]) offset, -1 = none
 };
+
+// the snapshots of the CAPACITY convergence exit are kept while they fit this
+// budget (j120-shape projects: ~20 KB; 300 activities with capacity ~80: off)
+constexpr int SNAP_MAX_BYTES = 48 * 1024;
 
 // big: some instance of the launch has a duration or fan-out above 32 -- only
 // then does the prefix-reusing TIME evaluator keep an undo log (2n words)
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
-                                               int rmax, int cap_lanes, int big = 1) {
+                                               int rmax, int cap_lanes, int big = 1,
+                                               bool snap = false) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
-  if (G == 32) return 2 * m * cap_row_stride(rmax) + n;  // c | c_pre | fin
+  if (G == 32) return (snap ? 1 : 2) * m * cap_row_stride(rmax) + n;  // c | c_pre | fin
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));
 }
 
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,
                                               int rmax, int delta, int T, int nwarps,
-                                              int cap_lanes = 32, int big = 1) {
+                                              int cap_lanes = 32, int big = 1, int sumcap = 0) {
   SmemPlan p;
   auto a4 = [](int x) { return (x + 3) & ~3; };
   int off = 0;
@@ -175,7 +181,14 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.red = off; off += 72;
   p.scal = off; off += SC_WORDS;
   p.cap_lanes = cap_lanes;
-  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big));
+  const bool snap = mode == MODE_CAPACITY && G == 32 && sumcap > 0 &&
+                    2ll * n * sumcap <= SNAP_MAX_BYTES;
+  p.snap = -1;
+  if (snap) {
+    p.snap = off;
+    off += a4((n * sumcap + 1) / 2);
+  }
+  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big, snap));
   p.evs = off; off += p.warp_words * nwarps;
   p.total = off;
   return p;
@@ -204,6 +217,7 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.red = smem + p.red;
   c.scal = smem + p.scal;
   c.evs = smem + p.evs;
+  c.snap = p.snap >= 0 ? smem + p.snap : nullptr;
   c.warp_words = p.warp_words;
   c.cap_lanes = p.cap_lanes;
   c.moves_buf = moves_buf;

@@ -78,6 +78,14 @@ __device__ __forceinline__ void sts64_if(bool p, uint32_t a, uint32_t x, uint32_
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v2.u32 [%1], {%2, %3};\n\t}"
                ::"r"(static_cast<uint32_t>(p)), "r"(a), "r"(x), "r"(y) : "memory");
 }
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
 // *a += v as one shared-memory reduction (no return value)
 __device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -777,18 +785,32 @@ __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, 
     cap_update_warp(a_row, capk, r, s, d);
 }
 
-// Alg. 4 for every resource the activity demands (lane k < m: capacity and
-// demand of resource k), one after another with the whole warp.
-__device__ __forceinline__ void cap_update_all(uint32_t a_c, int rs, int m, int capk, int req,
+// Alg. 4 for every resource the activity demands (lane k < m: capacity,
+// demand and row offset -- in words from a_c -- of resource k), one after
+// another with the whole warp.
+__device__ __forceinline__ void cap_update_all(uint32_t a_c, int off, int m, int capk, int req,
                                                int start, int dur) {
   const int lane = threadIdx.x & 31;
   unsigned used = __ballot_sync(FULL_MASK, lane < m && req > 0);
   while (used) {
     const int k = __ffs(used) - 1;
     used &= used - 1;
-    cap_update_row(a_c + 4 * k * rs, __shfl_sync(FULL_MASK, capk, k),
+    cap_update_row(a_c + 4 * __shfl_sync(FULL_MASK, off, k), __shfl_sync(FULL_MASK, capk, k),
                    __shfl_sync(FULL_MASK, req, k), start, dur);
   }
+}
+
+// compact state layout: row k starts at the sum of the capacities before it
+// (lane k < m gets its row's offset; S = the sum of all capacities)
+__device__ __forceinline__ int cap_row_offset(int capk) {
+  const int lane = threadIdx.x & 31;
+  int x = capk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - capk;
 }
 
 // Eq. 7 start (kernels.py:68-78, also for zero durations, as kernels.py:
@@ -797,7 +819,7 @@ __device__ __forceinline__ void cap_update_all(uint32_t a_c, int rs, int m, int 
 // packed: the record's demand word holds every demand as an 8-bit lane (one
 // packing word, 8-bit lanes: m <= 4), so no demand load is needed.
 __device__ __forceinline__ int cap_start_warp(int act, int esv, uint32_t a_dem, int m, int capk,
-                                              int rs, uint32_t a_c, int& req,
+                                              int off, uint32_t a_c, int& req,
                                               bool packed = false, uint32_t dword = 0u) {
   const int lane = threadIdx.x & 31;
   int t = 0;
@@ -805,7 +827,7 @@ __device__ __forceinline__ int cap_start_warp(int act, int esv, uint32_t a_dem, 
   if (lane < m) {
     req = packed ? static_cast<int>((dword >> (8 * lane)) & 0xffu)
                  : static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
-    if (req > 0) t = static_cast<int>(lds32(a_c + 4 * (lane * rs + capk - req)));
+    if (req > 0) t = static_cast<int>(lds32(a_c + 4 * (off + capk - req)));
   }
   return max(esv, __reduce_max_sync(FULL_MASK, t));
 }
@@ -814,12 +836,12 @@ __device__ __forceinline__ int cap_start_warp(int act, int esv, uint32_t a_dem, 
 // the finish time pushed to the successors' es.
 //   capk: lane k < m holds resource k's capacity (lanes >= m: 0)
 __device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t a_dem, int m,
-                                             int capk, int rs, uint32_t a_c, uint32_t a_push,
+                                             int capk, int off, uint32_t a_c, uint32_t a_push,
                                              int e0, int ecnt, uint32_t a_es, int& cmax) {
   const int lane = threadIdx.x & 31;
   int req;
-  const int start = cap_start_warp(act, esv, a_dem, m, capk, rs, a_c, req);
-  if (dur > 0) cap_update_all(a_c, rs, m, capk, req, start, dur);
+  const int start = cap_start_warp(act, esv, a_dem, m, capk, off, a_c, req);
+  if (dur > 0) cap_update_all(a_c, off, m, capk, req, start, dur);
   const int fin = start + dur;
   cmax = max(cmax, fin);
   for (int e = lane; e < ecnt; e += 32) red_max_shared(a_es + 4 * lds32(a_push + 4 * (e0 + e)), fin);
@@ -829,24 +851,33 @@ __device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t
 
 // Whole schedule of the order at a_ord (one warp); starts_out may be null.
 //   a_info: per-activity records (dur, -, push span, -); a_push: push targets
+//   scratch: c (compact rows, S = sum of capacities <= m * rs words) | es [n]
+//   snap (optional): the state after every position, uint16 [n][S] at this
+//   shared address -- the CAPACITY evaluator's convergence test reads it
 __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, uint32_t a_dem,
                                             const int* cap, int n, int m, int rs, uint32_t a_scr,
-                                            uint32_t a_ord, int* __restrict__ starts_out) {
+                                            uint32_t a_ord, int* __restrict__ starts_out,
+                                            uint32_t a_snap = 0u) {
   const int lane = threadIdx.x & 31;
+  const int capk = lane < m ? cap[lane] : 0;
+  const int off = cap_row_offset(capk);
+  const int S = __shfl_sync(FULL_MASK, off + capk, 31);  // lanes >= m: capk 0
   const uint32_t a_c = a_scr, a_es = a_scr + 4 * m * rs;
-  for (int j = lane; j < m * rs; j += 32) sts32(a_c + 4 * j, 0);
+  for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, 0);
   for (int a = lane; a < n; a += 32) sts32(a_es + 4 * a, 0);
   __syncwarp();
-  const int capk = lane < m ? cap[lane] : 0;
   int cmax = 0;
   for (int pos = 0; pos < n; ++pos) {
     const int act = static_cast<int>(lds32(a_ord + 4 * pos));
     const int4 rec = lds128(a_info + 16 * act);
     const int esv = static_cast<int>(lds32(a_es + 4 * act));
-    const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, rs, a_c, a_push,
+    const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, off, a_c, a_push,
                                 rec.z & 0xffff, rec.z >> 16, a_es, cmax);
     if (starts_out && lane == 0) starts_out[act] = s;
+    if (a_snap)
+      for (int j = lane; j < S; j += 32) sts16(a_snap + 2 * (pos * S + j), lds32(a_c + 4 * j));
   }
+  __syncwarp();
   return cmax;
 }
 

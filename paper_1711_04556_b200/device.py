@@ -29,7 +29,8 @@ MODE_CAPACITY = 0
 MODE_TIME = 1
 BLOB_MAGIC = 0x52435053
 HDR = 32
-(B_MAGIC, B_N, B_M, B_H, B_E, B_W, B_LB, B_RMAX, B_CPM, B_LEN, B_NLVL, B_BIG) = range(12)
+(B_MAGIC, B_N, B_M, B_H, B_E, B_W, B_LB, B_RMAX, B_CPM, B_LEN, B_NLVL, B_BIG,
+ B_SUMCAP) = range(13)
 (B_OFF_DUR, B_OFF_DEM, B_OFF_CAP, B_OFF_PPTR, B_OFF_PDAT, B_OFF_SPTR, B_OFF_SDAT, B_OFF_REQ,
  B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT) = range(16, 27)
 
@@ -490,6 +491,7 @@ class BatchSolver:
         self.m_max = max(int(b[B_M]) for b in blobs)
         self.rmax_max = max(int(b[B_RMAX]) for b in blobs)
         self.no_big = int(not any(int(b[B_BIG]) for b in blobs))
+        self.sumcap_max = max(int(b[B_SUMCAP]) for b in blobs)
         self.nbhd_max = max(1, max(neighborhood_size(int(b[B_N]), cfg.delta) for b in blobs))
         if self.nbhd_max >= KEY_LIMIT:
             raise UnsupportedInstance(f"neighbourhood of {self.nbhd_max} moves >= {KEY_LIMIT}")
@@ -602,6 +604,7 @@ class BatchSolver:
                      else pick_cluster(n_group * cfg.workers))
         a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
         a.no_big = self.no_big
+        a.sumcap_max = self.sumcap_max
         a.t0_ns = ptr(self.t0)
         if self.peer is not None:
             self.peer.fill_args(a)

@@ -132,10 +132,11 @@ def _gpu_worker(rank: int, world: int, port: int, kind: str, out):
     from paper_1711_04556_b200 import evaluate, synth
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     from paper_1711_04556_b200.population import PeerExchange
-    insts = synth.benchmark_batch("j60p", 6, first_seed=20)
+    # the hardest grid cell (RS 0.1): the pools do not start at the critical path
+    insts = synth.benchmark_batch("j120p", 6, first_seed=0)
     res = {}
     if kind == "epochs":
-        cfg = SolveConfig(total_iters=200, workers=2, pool_size=8, tabu_size=250, delta=60,
+        cfg = SolveConfig(total_iters=200, workers=2, pool_size=8, tabu_size=800, delta=60,
                           phi_steps=20, phi_max=3, seed=1000 * rank)
         s = BatchSolver(insts, [1] * 6, cfg)
         s.upload()
@@ -146,7 +147,7 @@ def _gpu_worker(rank: int, world: int, port: int, kind: str, out):
         res["rounds"] = ex.rounds
     else:
         iters = 2000 if rank == 1 else 5
-        cfg = SolveConfig(total_iters=iters, workers=1, pool_size=8, tabu_size=250, delta=60,
+        cfg = SolveConfig(total_iters=iters, workers=1, pool_size=8, tabu_size=800, delta=60,
                           phi_steps=20, phi_max=3, seed=1000 * rank)
         s = BatchSolver(insts, [1] * 6, cfg)
         peer = PeerExchange(s, poll_every=1)

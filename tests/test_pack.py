@@ -58,9 +58,9 @@ def reference_blob(inst) -> np.ndarray:
     fan = max([len(s) for s in inst.successors]
               + [len(p) for i, p in enumerate(inst.predecessors) if not (sink_free and i == n - 1)]
               + [0])
-    hdr[:12] = [0x52435053, n, m, int(ka.horizon), len(ka.pred_dat), W, lb,
+    hdr[:13] = [0x52435053, n, m, int(ka.horizon), len(ka.pred_dat), W, lb,
                 max(1, top), critical_path_length(inst), off, len(levels),
-                int(int(dur.max()) > 32 or fan > 32)]
+                int(int(dur.max()) > 32 or fan > 32), int(cap.sum())]
     return np.concatenate([hdr] + [np.asarray(p, np.int32) for p in parts])
 
 
@@ -87,8 +87,9 @@ def test_pack_matches_layout_restatement(ginst):
         assert got.dtype == np.int32
         assert got.tolist() == want.tolist(), inst.name
         sh = device.blob_shape(got)
-        assert (sh.n, sh.m, sh.horizon, sh.edges, sh.words, sh.rmax, sh.cpm, sh.len, sh.big) == (
-            got[1], got[2], got[3], got[4], got[5], got[7], got[8], len(got), got[11])
+        assert (sh.n, sh.m, sh.horizon, sh.edges, sh.words, sh.rmax, sh.cpm, sh.len, sh.big,
+                sh.sumcap) == (got[1], got[2], got[3], got[4], got[5], got[7], got[8], len(got),
+                               got[11], got[12])
 
 
 def test_pack_errors():
