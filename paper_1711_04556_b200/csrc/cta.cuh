@@ -29,8 +29,10 @@ struct CtaCtx {
   int* red;        // [72] reduction scratch
   int* scal;       // [SC_WORDS]
   int* evs;        // evaluation scratch (per warp)
-  int* snap;       // CAPACITY: uint16 [n][S] state after every position of the
-                   // current schedule (convergence exit), or null
+  int* snap;       // CAPACITY group 32: uint16 [n/k][S] state after every k-th
+                   // position of the current schedule (move starts, convergence)
+  int snap_words;  // its capacity (32-bit words)
+  int snap_k, snap_S;  // this instance's stride k and state size S
   int warp_words;  // evaluation scratch words per warp
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)
   bool inc;        // TIME G = 32: reuse the current order's schedule prefix
@@ -41,6 +43,18 @@ struct CtaCtx {
   int* cmax_buf;        // global [nbhd] makespans
   int* err;
 };
+
+// the snapshot stride of the staged instance: k = 1 unless n*S uint16 exceed
+// the plan's snapshot capacity (all threads call; no barrier needed)
+__device__ __forceinline__ void cta_snap_stride(CtaCtx& c) {
+  int S = 0;
+  for (int k = 0; k < c.I.m; ++k) S += c.I.cap[k];
+  const int cap16 = 2 * c.snap_words;
+  int k = 1;
+  while (k < c.I.n && (c.I.n / k) * S > cap16) ++k;
+  c.snap_S = S;
+  c.snap_k = k;
+}
 
 // ---------------------------------------------------------------- block ops
 

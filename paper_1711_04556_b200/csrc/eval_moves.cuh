@@ -313,22 +313,23 @@ __device__ __noinline__ void eval_moves_split(int o_info, int o_pull, int o_req,
 // (its start, max(es, Eq. 7), is bounded by the finish times already in the
 // makespan).
 //
-// SNAP: the current schedule's state after every position is in shared
-// memory (uint16 [n][S], written by the base pass, o_snap).  A move then
-// starts from the snapshot at u-1 (no prefix state to extend), and if every
-// activity at positions u..v starts where it does in the current schedule
-// AND the state after v equals the snapshot at v, the rest of the schedule is
-// the current one: C_max = base_cmax (convergence exit).  Capacity-indexed
-// states depend on the order of the updates, so the state is compared, not
-// implied by the starts as in TIME.
-// !SNAP (large n*S): each warp extends a prefix state c_pre with the known
-// starts as u grows and copies it per move; no convergence exit.
-//   per-warp scratch: c [S] | c_pre [S] (!SNAP) | fin [n]; S <= m*rs
+// The current schedule's state after every k-th position (positions k-1,
+// 2k-1, ...; k = 1 unless n*S exceeds the snapshot budget) is in shared
+// memory (uint16 [n/k][S], written by the base pass, o_snap).  A move starts
+// from the latest snapshot before u and replays the few positions up to u-1
+// with their known starts.  If every activity at positions u..p (p >= v, a
+// snapshot position) starts where it does in the current schedule AND the
+// state after p equals the snapshot, the rest of the schedule is the current
+// one: C_max = base_cmax (convergence exit).  Capacity-indexed states depend
+// on the order of the updates, so the state is compared, not implied by the
+// starts as in TIME -- and it may only agree a few positions after v, once
+// the differing entries have been overwritten.
+//   per-warp scratch: c [S] | fin [n]  (S <= m*rs)
 //   o_info: pull records (info_r); o_pull: padded predecessor lists (pdat)
-template <bool BIG, bool SNAP>
+template <bool BIG>
 __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_dem, int o_cap,
                                                  int o_base, int o_bst, int o_ctr, int o_evs,
-                                                 int o_snap, int n, int m, int rs,
+                                                 int o_snap, int snap_k, int n, int m, int rs,
                                                  const uint32_t* __restrict__ moves,
                                                  int* __restrict__ cmax_out, int n_feas,
                                                  int warp_words, bool reuse, uint32_t ctr_cl,
@@ -337,18 +338,19 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
   const int capk = lane < m ? dsm[o_cap + lane] : 0;
   const int off = cap_row_offset(capk);
   const int S = __shfl_sync(FULL_MASK, off + capk, 31);
-  const int mr = m * rs;  // >= S: the scratch layout's row budget
   const uint32_t a_scr = sa(dsm + o_evs + warp * warp_words);
-  const uint32_t a_c = a_scr, a_cp = a_c + 4 * mr, a_fin = a_cp + (SNAP ? 0u : 4u * mr);
+  const uint32_t a_c = a_scr, a_fin = a_c + 4 * m * rs;
   const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_dem = sa(dsm + o_dem),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
-                 a_snap = SNAP ? sa(dsm + o_snap) : 0u;
+                 a_snap = sa(dsm + o_snap);
   const uint32_t a_pdat_l = opaque(a_pdat + 4 * lane);
-  if (!SNAP)
-    for (int j = lane; j < S; j += 32) sts32(a_cp + 4 * j, 0);
-  __syncwarp();
   const int pend = lds128(a_info + 16 * static_cast<int>(lds32(a_base + 4 * (n - 1)))).x == 0
                        ? n - 1 : n;
+  auto demand = [&](int act, const int4& rec) {  // lane k < m: resource k's demand
+    if (lane >= m) return 0;
+    return packed ? static_cast<int>((static_cast<uint32_t>(rec.y) >> (8 * lane)) & 0xffu)
+                  : static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
+  };
   int up = 0, cm_pre = 0, steps = 0;
   for (;;) {
     int idx = 0;
@@ -358,37 +360,35 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
     const uint32_t mv = moves[idx];
     const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
     const int u0 = reuse ? u : 0;
-    // ---- positions < u0: the current schedule's finish times (and, !SNAP,
-    // its state extended with the known starts)
+    // ---- positions < u0: the current schedule's finish times
     for (; up < u0; ++up) {
       const int act = static_cast<int>(lds32(a_base + 4 * up));
-      const int4 rec = lds128(a_info + 16 * act);
-      const int st = static_cast<int>(lds32(a_bst + 4 * act));
-      if (!SNAP && rec.x > 0) {
-        int req = 0;
-        if (lane < m)
-          req = packed ? static_cast<int>((static_cast<uint32_t>(rec.y) >> (8 * lane)) & 0xffu)
-                       : static_cast<int>(lds32(a_dem + 4 * (act * m + lane)));
-        cap_update_all(a_cp, off, m, capk, req, st, rec.x);
-      }
-      cm_pre = max(cm_pre, st + rec.x);
-      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(st + rec.x));
-      __syncwarp();
+      const int fin = static_cast<int>(lds32(a_bst + 4 * act)) + lds128(a_info + 16 * act).x;
+      cm_pre = max(cm_pre, fin);
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
     }
-    if (SNAP && u0 > 0) {
-      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, lds16(a_snap + 2 * ((u0 - 1) * S + j)));
-    } else if (SNAP) {
-      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, 0);
-    } else {
-      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, lds32(a_cp + 4 * j));
-    }
+    // ---- the state after u0 - 1: the latest snapshot, then the positions
+    // after it replayed with their known starts
+    const int q = u0 / snap_k;  // snapshots 0..q-1 cover positions < q*k
+    if (q > 0)
+      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, lds16(a_snap + 2 * ((q - 1) * S + j)));
+    else
+      for (int j = lane; j < S; j += 32) sts32(a_c + 4 * j, 0u);
     __syncwarp();
+    for (int p = q * snap_k; p < u0; ++p) {
+      const int act = static_cast<int>(lds32(a_base + 4 * p));
+      const int4 rec = lds128(a_info + 16 * act);
+      if (rec.x > 0)
+        cap_update_all(a_c, off, m, capk, demand(act, rec),
+                       static_cast<int>(lds32(a_bst + 4 * act)), rec.x);
+    }
+    steps += u0 - q * snap_k;
     // ---- positions u0.. of the swapped order
     int cm = cm_pre, p = u0;
-    bool div = !SNAP || !reuse;
+    bool div = !reuse;
     for (; p < pend; ++p) {
-      const int q = p == u ? v : (p == v ? u : p);
-      const int act = static_cast<int>(lds32(a_base + 4 * q));
+      const int qq = p == u ? v : (p == v ? u : p);
+      const int act = static_cast<int>(lds32(a_base + 4 * qq));
       const int4 rec = lds128(a_info + 16 * act);
       const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
       int f = static_cast<int>(lds32(a_fin + 4 * lds32(a_pdat_l + 4 * p0)));
@@ -404,23 +404,22 @@ __device__ __noinline__ void eval_moves_cap_warp(int o_info, int o_pull, int o_d
       const int fin = start + rec.x;
       cm = max(cm, fin);
       sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
-      if (SNAP && !div) {
+      if (!div) {
         div = start != static_cast<int>(lds32(a_bst + 4 * act));
-        if (!div && p == v) {  // same starts through v: compare the state
+        if (!div && p >= v && p % snap_k == snap_k - 1) {  // compare with the snapshot
           __syncwarp();
           bool diff = false;
           for (int j = lane; j < S; j += 32)
-            diff |= lds32(a_c + 4 * j) != lds16(a_snap + 2 * (v * S + j));
+            diff |= lds32(a_c + 4 * j) != lds16(a_snap + 2 * ((p / snap_k) * S + j));
           if (!__any_sync(FULL_MASK, diff)) {
             ++p;
             break;  // converged: the rest is the current schedule
           }
-          div = true;
         }
       }
       __syncwarp();
     }
-    if (lane == 0) cmax_out[idx] = (SNAP && !div) ? base_cmax : cm;
+    if (lane == 0) cmax_out[idx] = div || p >= pend ? cm : base_cmax;
     steps += p - u0;
   }
   if (lane == 0) {
@@ -582,30 +581,21 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
 }
 
 // the prefix-reusing CAPACITY warp evaluator on this CTA's copy of the current order
-template <bool BIG>
-__device__ __forceinline__ void eval_moves_cap_warp_snap(const CtaCtx& c, int n_feas, bool reuse,
-                                                         uint32_t ctr_cl, int base_cmax) {
-  if (c.snap)
-    eval_moves_cap_warp<BIG, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem),
-                                   soff(c.I.cap), soff(c.base), soff(c.bst),
-                                   soff(c.scal + SC_CTR), soff(c.evs), soff(c.snap), c.I.n, c.I.m,
-                                   cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
-                                   c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I), base_cmax);
-  else
-    eval_moves_cap_warp<BIG, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem),
-                                    soff(c.I.cap), soff(c.base), soff(c.bst),
-                                    soff(c.scal + SC_CTR), soff(c.evs), 0, c.I.n, c.I.m,
-                                    cap_row_stride(c.I.rmax), c.moves_buf, c.cmax_buf, n_feas,
-                                    c.warp_words, reuse, ctr_cl, cap_demand_packed(c.I),
-                                    base_cmax);
-}
 __device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
                                                              bool reuse, uint32_t ctr_cl,
                                                              int base_cmax) {
   if (c.I.big)
-    eval_moves_cap_warp_snap<true>(c, n_feas, reuse, ctr_cl, base_cmax);
+    eval_moves_cap_warp<true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
+                              soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
+                              soff(c.snap), c.snap_k, c.I.n, c.I.m, cap_row_stride(c.I.rmax),
+                              c.moves_buf, c.cmax_buf, n_feas, c.warp_words, reuse, ctr_cl,
+                              cap_demand_packed(c.I), base_cmax);
   else
-    eval_moves_cap_warp_snap<false>(c, n_feas, reuse, ctr_cl, base_cmax);
+    eval_moves_cap_warp<false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.dem), soff(c.I.cap),
+                               soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
+                               soff(c.snap), c.snap_k, c.I.n, c.I.m, cap_row_stride(c.I.rmax),
+                               c.moves_buf, c.cmax_buf, n_feas, c.warp_words, reuse, ctr_cl,
+                               cap_demand_packed(c.I), base_cmax);
 }
 
 // Cluster follower (rank > 0): evaluates moves of the leader's neighbourhood
@@ -635,11 +625,11 @@ __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, 
       c.base[p] = static_cast<int>(ld_cluster(l_base + 4 * p));
       c.bst[p] = static_cast<int>(ld_cluster(l_bst + 4 * p));
     }
-    if (MODE == MODE_CAPACITY && c.snap) {  // the current schedule's state snapshots
-      int S = 0;
-      for (int k = 0; k < c.I.m; ++k) S += c.I.cap[k];
+    if (MODE == MODE_CAPACITY && G == 32) {  // the current schedule's state snapshots
+      __syncthreads();  // a re-staged instance's capacities are in place
+      cta_snap_stride(c);
       const uint32_t l_snap = cluster_map(sa(c.snap), 0);
-      for (int w = tid; w < (c.I.n * S + 1) / 2; w += blockDim.x)
+      for (int w = tid; w < ((c.I.n / c.snap_k) * c.snap_S + 1) / 2; w += blockDim.x)
         c.snap[w] = static_cast<int>(ld_cluster(l_snap + 4 * w));
     }
     __syncthreads();
@@ -705,8 +695,8 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
       int cm = 0;
       if (c.inc)
         cm = sgs_cap_warp(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.dem), c.I.cap, c.I.n, c.I.m,
-                          cap_row_stride(c.I.rmax), sa(c.evs), sa(c.base), c.bst,
-                          c.snap ? sa(c.snap) : 0u);
+                          cap_row_stride(c.I.rmax), sa(c.evs), sa(c.base), c.bst, sa(c.snap),
+                          c.snap_k);
       if (lane == 0) {
         c.scal[SC_CTR] = 0;
         c.scal[SC_STEPS] = c.inc ? c.I.n : 0;

@@ -913,6 +913,7 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
         if (tid == 0) set_err(A.err, DE_SMEM);
         break;
       }
+      if (c.snap) cta_snap_stride(c);
       cta_init_rows(c);
       continue;
     }

@@ -143,12 +143,13 @@ __device__ void cta_diversify(CtaCtx& c, int* work, int steps, Pcg64& rng) {
 struct SmemPlan {
   int inst, base, pos, msp, mpp, rs, best, rowc, bst, tabu_list, tabu_cnt, red, scal, evs;
   int warp_words, total, cap_lanes;
-  int snap;  // CAPACITY group 32: state snapshots (uint16 [n][S]) offset, -1 = none
+  int snap, snap_words;  // CAPACITY group 32: state snapshots (uint16), -1 / 0 = none
 };
 
-// the snapshots of the CAPACITY convergence exit are kept while they fit this
-// budget (j120-shape projects: ~20 KB; 300 activities with capacity ~80: off)
-constexpr int SNAP_MAX_BYTES = 48 * 1024;
+// shared-memory budget of the CAPACITY evaluator's state snapshots: an
+// instance whose n*S uint16 exceed it keeps every k-th position's state
+// (j120-shape projects: k = 1; 300 activities with capacities ~80: k = 3)
+constexpr int SNAP_MAX_BYTES = 40 * 1024;
 
 // big: some instance of the launch has a duration or fan-out above 32 -- only
 // then does the prefix-reusing TIME evaluator keep an undo log (2n words)
@@ -156,7 +157,7 @@ __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, in
                                                int rmax, int cap_lanes, int big = 1,
                                                bool snap = false) {
   if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
-  if (G == 32) return (snap ? 1 : 2) * m * cap_row_stride(rmax) + n;  // c | c_pre | fin
+  if (G == 32) return m * cap_row_stride(rmax) + n;  // c | fin (snapshots: CTA-wide)
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));
 }
@@ -181,12 +182,15 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.red = off; off += 72;
   p.scal = off; off += SC_WORDS;
   p.cap_lanes = cap_lanes;
-  const bool snap = mode == MODE_CAPACITY && G == 32 && sumcap > 0 &&
-                    2ll * n * sumcap <= SNAP_MAX_BYTES;
+  const bool snap = mode == MODE_CAPACITY && G == 32;
   p.snap = -1;
+  p.snap_words = 0;
   if (snap) {
+    long long need = (static_cast<long long>(n) * (sumcap > 0 ? sumcap : m * rmax) + 1) / 2;
+    if (need > SNAP_MAX_BYTES / 4) need = SNAP_MAX_BYTES / 4;
     p.snap = off;
-    off += a4((n * sumcap + 1) / 2);
+    p.snap_words = a4(static_cast<int>(need));
+    off += p.snap_words;
   }
   p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big, snap));
   p.evs = off; off += p.warp_words * nwarps;
@@ -218,12 +222,16 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.scal = smem + p.scal;
   c.evs = smem + p.evs;
   c.snap = p.snap >= 0 ? smem + p.snap : nullptr;
+  c.snap_words = p.snap_words;
+  c.snap_k = 1;
+  c.snap_S = 0;
   c.warp_words = p.warp_words;
   c.cap_lanes = p.cap_lanes;
   c.moves_buf = moves_buf;
   c.cmax_buf = cmax_buf;
   c.err = err;
   __syncthreads();
+  if (c.snap) cta_snap_stride(c);
   cta_init_rows(c);
 }
 

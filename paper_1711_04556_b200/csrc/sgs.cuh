@@ -695,92 +695,69 @@ __device__ __forceinline__ void cap_update_warp(uint32_t a_row, int capk, int r,
   __syncwarp();
 }
 
-// cap_update_warp for rows of up to 32*K entries and demands r < 32: the row
-// is read once into K registers per lane (entry 32k + lane in v[k]); the
-// shifted value c[i - r] comes from the lane r to the left (one chunk back
-// for lanes < r), the scan and the writes run on registers -- one LDS and one
-// STS per entry instead of the generic path's re-reads.
-template <int K>
-__device__ __forceinline__ void cap_update_reg(uint32_t a_row, int capk, int r, int s, int d) {
+// cap_update_warp for demands r < 32 on a 32-entry window starting at i0:
+// lane l holds c[i0 + l], the shifted value c[i0 + l - r] is one shuffle
+// away, and one warp-wide scan finds the stop t -- which lies within the
+// window unless the surplus outlasts 32 - r entries past i0 + r (then the
+// generic form runs instead; nothing has been written yet).  Rows up to 32
+// entries are read once (the window is a shuffle of the row).
+__device__ __forceinline__ void cap_update_win(uint32_t a_row, int capk, int r, int s, int d) {
   const int lane = threadIdx.x & 31;
   const int T = s + d;
-  int v[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = 32 * k + lane;
-    v[k] = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-  }
-  int i0 = capk, c0 = 0;
-#pragma unroll
-  for (int k = K - 1; k >= 0; --k) {  // the lowest chunk holding an entry < T decides
-    const unsigned msk = __ballot_sync(FULL_MASK, 32 * k + lane < capk && v[k] < T);
+  int i0 = capk, c0 = 0, v0 = 0;
+  for (int b = 0; b < capk; b += 32) {
+    const int i = b + lane;
+    const int v = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+    if (b == 0) v0 = v;
+    const unsigned msk = __ballot_sync(FULL_MASK, i < capk && v < T);
     if (msk) {
       const int l = __ffs(msk) - 1;
-      i0 = 32 * k + l;
-      c0 = __shfl_sync(FULL_MASK, v[k], l);
+      i0 = b + l;
+      c0 = __shfl_sync(FULL_MASK, v, l);
+      break;
     }
   }
   if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
+  const int i = i0 + lane;
+  const bool in = i < capk;
   if (c0 <= s) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int i = 32 * k + lane;
-      if (i >= i0 && i < i0 + r) sts32(a_row + 4 * i, static_cast<uint32_t>(T));
-    }
+    if (lane < r) sts32(a_row + 4 * i, static_cast<uint32_t>(T));
     __syncwarp();
     return;
   }
-  int oir[K];
-  int carry = 0, t = capk, newt = 0;
-  bool done = false;
-  const int srcl = (lane - r) & 31;
+  // the window c[i0 .. i0+31]
+  int w;
+  if (capk <= 32)
+    w = __shfl_sync(FULL_MASK, v0, i & 31);
+  else
+    w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+  const int oir = __shfl_sync(FULL_MASK, w, (lane - r) & 31);  // c[i - r] for lane >= r
+  const int f = max(w, s);
+  const int g = in ? (lane < r ? s - f : oir - f) : 0;
+  int S = g;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = 32 * k + lane;
-    const int a = __shfl_sync(FULL_MASK, v[k], srcl);
-    const int b = k > 0 ? __shfl_sync(FULL_MASK, v[k > 0 ? k - 1 : 0], srcl) : 0;
-    oir[k] = lane >= r ? a : b;  // c[i - r]
-    if (!done) {
-      const bool in = i < capk, sh = i >= i0 + r;
-      const int f = max(v[k], s);
-      const int g = (in && i >= i0) ? (sh ? oir[k] - f : s - f) : 0;
-      int S = g;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL_MASK, S, o);
-        if (lane >= o) S += y;
-      }
-      S += carry;
-      const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
-      if (term) {
-        const int l = __ffs(term) - 1;
-        t = 32 * k + l;
-        newt = __shfl_sync(FULL_MASK, f - (S - g), l);
-        done = true;
-      } else {
-        carry = __shfl_sync(FULL_MASK, S, 31);
-      }
-    }
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, S, o);
+    if (lane >= o) S += y;
   }
-  const int end = t < capk ? t : capk;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = 32 * k + lane;
-    if (i >= i0 && i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : oir[k]));
-    if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+  const unsigned term = __ballot_sync(FULL_MASK, in && lane >= r && S >= 0);
+  if (!term && i0 + 32 < capk) {  // the stop lies past the window (rare)
+    cap_update_warp(a_row, capk, r, s, d);
+    return;
   }
+  const int tl = term ? __ffs(term) - 1 : 32;  // no stop: the shift runs to the row's end
+  const int newt = __shfl_sync(FULL_MASK, f - (S - g), tl & 31);
+  __syncwarp();
+  if (in && lane < tl) sts32(a_row + 4 * i, static_cast<uint32_t>(lane < r ? T : oir));
+  if (lane == tl) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
   __syncwarp();
 }
 
-// Alg. 4 on one row: the register-resident form for rows up to 96 entries
-// and demands below 32, else the generic one.
+// Alg. 4 on one row: the window form for demands below 32, else the generic
+// one.
 __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
-  if (r < 32 && capk <= 32)
-    cap_update_reg<1>(a_row, capk, r, s, d);
-  else if (r < 32 && capk <= 64)
-    cap_update_reg<2>(a_row, capk, r, s, d);
-  else if (r < 32 && capk <= 96)
-    cap_update_reg<3>(a_row, capk, r, s, d);
+  if (r < 32)
+    cap_update_win(a_row, capk, r, s, d);
   else
     cap_update_warp(a_row, capk, r, s, d);
 }
@@ -852,12 +829,13 @@ __device__ __forceinline__ int cap_step_warp(int act, int dur, int esv, uint32_t
 // Whole schedule of the order at a_ord (one warp); starts_out may be null.
 //   a_info: per-activity records (dur, -, push span, -); a_push: push targets
 //   scratch: c (compact rows, S = sum of capacities <= m * rs words) | es [n]
-//   snap (optional): the state after every position, uint16 [n][S] at this
-//   shared address -- the CAPACITY evaluator's convergence test reads it
+//   snap (optional): the state after every k-th position (positions k-1,
+//   2k-1, ...), uint16 [n/k][S] at this shared address -- the CAPACITY
+//   evaluator starts its moves from them and tests convergence against them
 __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, uint32_t a_dem,
                                             const int* cap, int n, int m, int rs, uint32_t a_scr,
                                             uint32_t a_ord, int* __restrict__ starts_out,
-                                            uint32_t a_snap = 0u) {
+                                            uint32_t a_snap = 0u, int snap_k = 1) {
   const int lane = threadIdx.x & 31;
   const int capk = lane < m ? cap[lane] : 0;
   const int off = cap_row_offset(capk);
@@ -874,8 +852,9 @@ __device__ __forceinline__ int sgs_cap_warp(uint32_t a_info, uint32_t a_push, ui
     const int s = cap_step_warp(act, rec.x, esv, a_dem, m, capk, off, a_c, a_push,
                                 rec.z & 0xffff, rec.z >> 16, a_es, cmax);
     if (starts_out && lane == 0) starts_out[act] = s;
-    if (a_snap)
-      for (int j = lane; j < S; j += 32) sts16(a_snap + 2 * (pos * S + j), lds32(a_c + 4 * j));
+    if (a_snap && pos % snap_k == snap_k - 1)
+      for (int j = lane; j < S; j += 32)
+        sts16(a_snap + 2 * ((pos / snap_k) * S + j), lds32(a_c + 4 * j));
   }
   __syncwarp();
   return cmax;
