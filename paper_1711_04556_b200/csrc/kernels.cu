@@ -67,7 +67,12 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
 // runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120);
 // the other evaluators keep 16 warps at 64 registers (at 56 the CAPACITY
 // thread evaluator spills: -16 % on j120)
-constexpr int ksolve_threads(int mode, int G) { return mode == MODE_TIME && G == 32 ? 576 : 512; }
+#ifndef CAP_THREADS
+#define CAP_THREADS 512
+#endif
+constexpr int ksolve_threads(int mode, int G) {
+  return mode == MODE_TIME && G == 32 ? 576 : (mode == MODE_CAPACITY && G == 32 ? CAP_THREADS : 512);
+}
 constexpr int KSOLVE_THREADS_MAX = 576;
 
 // =========================================================================

@@ -695,20 +695,20 @@ __device__ __forceinline__ void cap_update_warp(uint32_t a_row, int capk, int r,
   __syncwarp();
 }
 
-// cap_update_warp for demands r < 32 on a 32-entry window starting at i0:
-// lane l holds c[i0 + l], the shifted value c[i0 + l - r] is one shuffle
-// away, and one warp-wide scan finds the stop t -- which lies within the
-// window unless the surplus outlasts 32 - r entries past i0 + r (then the
-// generic form runs instead; nothing has been written yet).  Rows up to 32
-// entries are read once (the window is a shuffle of the row).
+// cap_update_warp on up to K 32-entry windows starting at i0 (entry i0 +
+// 32k + lane in lane `lane` of window k): each window is read once, the
+// shifted value c[i - r] is a shuffle within window 0 for demands below 32
+// and a load otherwise, one warp-wide scan per window finds the stop t, and
+// the writes follow once every read is done.  If the surplus outlasts the K
+// windows the generic form runs instead (nothing has been written yet).
+template <int K>
 __device__ __forceinline__ void cap_update_win(uint32_t a_row, int capk, int r, int s, int d) {
   const int lane = threadIdx.x & 31;
   const int T = s + d;
-  int i0 = capk, c0 = 0, v0 = 0;
+  int i0 = capk, c0 = 0;
   for (int b = 0; b < capk; b += 32) {
     const int i = b + lane;
     const int v = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-    if (b == 0) v0 = v;
     const unsigned msk = __ballot_sync(FULL_MASK, i < capk && v < T);
     if (msk) {
       const int l = __ffs(msk) - 1;
@@ -718,48 +718,71 @@ __device__ __forceinline__ void cap_update_win(uint32_t a_row, int capk, int r, 
     }
   }
   if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
-  const int i = i0 + lane;
-  const bool in = i < capk;
   if (c0 <= s) {
-    if (lane < r) sts32(a_row + 4 * i, static_cast<uint32_t>(T));
+    for (int j = lane; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
     __syncwarp();
     return;
   }
-  // the window c[i0 .. i0+31]
-  int w;
-  if (capk <= 32)
-    w = __shfl_sync(FULL_MASK, v0, i & 31);
-  else
-    w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-  const int oir = __shfl_sync(FULL_MASK, w, (lane - r) & 31);  // c[i - r] for lane >= r
-  const int f = max(w, s);
-  const int g = in ? (lane < r ? s - f : oir - f) : 0;
-  int S = g;
+  int ov[K];
+  int carry = 0, t = capk, newt = 0, last = -1;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL_MASK, S, o);
-    if (lane >= o) S += y;
+  for (int k = 0; k < K; ++k) {
+    if (last < 0) {
+      const int i = i0 + 32 * k + lane;
+      const bool in = i < capk, sh = i >= i0 + r;
+      const int w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+      int o;
+      if (k == 0 && r < 32)
+        o = __shfl_sync(FULL_MASK, w, (lane - r) & 31);
+      else
+        o = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
+      ov[k] = o;
+      const int f = max(w, s);
+      const int g = in ? (sh ? o - f : s - f) : 0;
+      int S = g;
+#pragma unroll
+      for (int q = 1; q < 32; q <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, S, q);
+        if (lane >= q) S += y;
+      }
+      S += carry;
+      const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
+      if (term) {
+        const int l = __ffs(term) - 1;
+        t = i0 + 32 * k + l;
+        newt = __shfl_sync(FULL_MASK, f - (S - g), l);
+        last = k;
+      } else if (i0 + 32 * (k + 1) >= capk) {
+        last = k;  // no stop: the shift runs to the row's end
+      } else {
+        carry = __shfl_sync(FULL_MASK, S, 31);
+      }
+    }
   }
-  const unsigned term = __ballot_sync(FULL_MASK, in && lane >= r && S >= 0);
-  if (!term && i0 + 32 < capk) {  // the stop lies past the window (rare)
+  if (last < 0) {  // the stop lies past the windows (rare)
     cap_update_warp(a_row, capk, r, s, d);
     return;
   }
-  const int tl = term ? __ffs(term) - 1 : 32;  // no stop: the shift runs to the row's end
-  const int newt = __shfl_sync(FULL_MASK, f - (S - g), tl & 31);
   __syncwarp();
-  if (in && lane < tl) sts32(a_row + 4 * i, static_cast<uint32_t>(lane < r ? T : oir));
-  if (lane == tl) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+  const int end = t < capk ? t : capk;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k <= last) {
+      const int i = i0 + 32 * k + lane;
+      if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : ov[k]));
+      if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+    }
+  }
   __syncwarp();
 }
 
-// Alg. 4 on one row: the window form for demands below 32, else the generic
-// one.
+// Alg. 4 on one row: one 32-entry window from i0 (demands below 32 with the
+// stop within the window -- the common case), else the generic form.  A/B on
+// B200 (tools/ab_args.sh, profiles/r2/cap_ab.txt): three windows held in
+// registers cost spills on the common path (-5 % j120p, -7 % j60p, +5 % on
+// the 300-activity set); 384 threads per CTA to avoid them: -13 %.
 __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
-  if (r < 32)
-    cap_update_win(a_row, capk, r, s, d);
-  else
-    cap_update_warp(a_row, capk, r, s, d);
+  cap_update_win<1>(a_row, capk, r, s, d);
 }
 
 // Alg. 4 for every resource the activity demands (lane k < m: capacity,
