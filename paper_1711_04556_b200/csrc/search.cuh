@@ -10,8 +10,8 @@
 //            CAP -> one thread per schedule (sgs.cuh)
 //   select   admissible = not tabu or C < aspiration; argmin over the packed
 //            key (C << 16 | rank) = lexicographic tie break (kernels.py:280-309)
-//   apply    swap + tabu_add on the shared-memory circular list with banded
-//            16-bit counters (kernels.py:263-277)
+//   apply    swap + tabu_add on the shared-memory circular list with a banded
+//            membership bitmap (kernels.py:263-277)
 #pragma once
 #include "common.cuh"
 #include "pcg64.cuh"
@@ -65,16 +65,19 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
     forced += forced_pick ? 1 : 0;
     const int pick = static_cast<int>(key & 0xffff);
     cur = static_cast<int>(key >> 16);
-    if (tid == 0) {
+    if (tid < 32) {  // warp 0: apply the move, tabu_add (kernels.py:263-277)
       const uint32_t mv = c.moves_buf[pick];
       const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
-      const int t = c.base[u];
-      c.base[u] = c.base[v];
-      c.base[v] = t;
-      c.scal[SC_HEAD] = tabu_add1(c, c.scal[SC_HEAD], u, v);
-      if (trace) trace[iters - 1] = cur;
-      c.scal[SC_BSTOK] = (c.cmax_buf[pick] & CONV_FLAG) ? 1 : 0;
-      c.scal[SC_FLAG] = budget_spent(c.budget_ns, c.t0_ns) ? 1 : 0;
+      const int head = tabu_add_warp(c, c.scal[SC_HEAD], u, v);
+      if (tid == 0) {
+        const int t = c.base[u];
+        c.base[u] = c.base[v];
+        c.base[v] = t;
+        c.scal[SC_HEAD] = head;
+        if (trace) trace[iters - 1] = cur;
+        c.scal[SC_BSTOK] = (c.cmax_buf[pick] & CONV_FLAG) ? 1 : 0;
+        c.scal[SC_FLAG] = budget_spent(c.budget_ns, c.t0_ns) ? 1 : 0;
+      }
     }
     __syncthreads();
     if (cur < local_best) {
@@ -178,7 +181,7 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
   p.rowc = off; off += a4(n);
   p.bst = off; off += a4(n);
   p.tabu_list = off; off += a4(T > 0 ? T : 1);
-  p.tabu_cnt = off; off += a4((n * (delta + 1) + 1) / 2);
+  p.tabu_cnt = off; off += a4((n * (delta + 1) + 31) / 32);  // membership bits
   p.red = off; off += 72;
   p.scal = off; off += SC_WORDS;
   p.cap_lanes = cap_lanes;
