@@ -18,7 +18,7 @@ enum { MODE_CAPACITY = 0, MODE_TIME = 1 };  // kernels.py:22-23
 
 enum BlobField {
   B_MAGIC = 0, B_N = 1, B_M = 2, B_H = 3, B_E = 4, B_W = 5, B_LB = 6, B_RMAX = 7, B_CPM = 8,
-  B_LEN = 9, B_NLVL = 10, B_BIG = 11, B_SUMCAP = 12,
+  B_LEN = 9, B_NLVL = 10, B_BIG = 11, B_SUMCAP = 12, B_LBRES = 13,
   B_OFF_DUR = 16, B_OFF_DEM = 17, B_OFF_CAP = 18, B_OFF_PPTR = 19, B_OFF_PDAT = 20,
   B_OFF_SPTR = 21, B_OFF_SDAT = 22, B_OFF_REQ = 23, B_OFF_CAPW = 24, B_OFF_LPTR = 25,
   B_OFF_LDAT = 26,

@@ -15,7 +15,8 @@
 // (instance.py:396-415: longest unit-weight distance from any root, ids
 // ascending inside a level), the B_BIG flag (a duration, fan-out or --
 // except into a zero-duration sink -- fan-in above 32) and B_SUMCAP (the sum
-// of the capacities: the compact capacity-indexed state's size).
+// of the capacities: the compact capacity-indexed state's size), B_LBRES (the
+// energy bound max_k ceil(sum_i d_i r_ik / R_k) of the makespan).
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -31,7 +32,7 @@ constexpr int kKeyLimit = 1 << 16;   // selection key packs (C_max << 16) | rank
 
 enum {
   B_MAGIC = 0, B_N = 1, B_M = 2, B_H = 3, B_E = 4, B_W = 5, B_LB = 6, B_RMAX = 7, B_CPM = 8,
-  B_LEN = 9, B_NLVL = 10, B_BIG = 11, B_SUMCAP = 12,
+  B_LEN = 9, B_NLVL = 10, B_BIG = 11, B_SUMCAP = 12, B_LBRES = 13,
   B_OFF_DUR = 16, B_OFF_DEM, B_OFF_CAP, B_OFF_PPTR, B_OFF_PDAT, B_OFF_SPTR, B_OFF_SDAT,
   B_OFF_REQ, B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT
 };
@@ -216,6 +217,16 @@ int rcpsp_pack_instance(const int32_t* dur, const int32_t* dem, const int32_t* c
   int sumcap = 0;
   for (int k = 0; k < m; ++k) sumcap += cap[k];
   blob[B_SUMCAP] = sumcap;
+  // resource (energy) lower bound of the makespan: max_k ceil(sum_i d_i r_ik / R_k)
+  long long lbres = 0;
+  for (int k = 0; k < m; ++k) {
+    if (cap[k] <= 0) continue;
+    long long e = 0;
+    for (int i = 0; i < n; ++i) e += static_cast<long long>(dur[i]) * dem[static_cast<size_t>(i) * m + k];
+    const long long b = (e + cap[k] - 1) / cap[k];
+    lbres = b > lbres ? b : lbres;
+  }
+  blob[B_LBRES] = static_cast<int32_t>(lbres);
   return 0;
 }
 

@@ -30,7 +30,7 @@ MODE_TIME = 1
 BLOB_MAGIC = 0x52435053
 HDR = 32
 (B_MAGIC, B_N, B_M, B_H, B_E, B_W, B_LB, B_RMAX, B_CPM, B_LEN, B_NLVL, B_BIG,
- B_SUMCAP) = range(13)
+ B_SUMCAP, B_LBRES) = range(14)
 (B_OFF_DUR, B_OFF_DEM, B_OFF_CAP, B_OFF_PPTR, B_OFF_PDAT, B_OFF_SPTR, B_OFF_SDAT, B_OFF_REQ,
  B_OFF_CAPW, B_OFF_LPTR, B_OFF_LDAT) = range(16, 27)
 

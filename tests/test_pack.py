@@ -58,9 +58,11 @@ def reference_blob(inst) -> np.ndarray:
     fan = max([len(s) for s in inst.successors]
               + [len(p) for i, p in enumerate(inst.predecessors) if not (sink_free and i == n - 1)]
               + [0])
-    hdr[:13] = [0x52435053, n, m, int(ka.horizon), len(ka.pred_dat), W, lb,
+    lbres = max([-(-int((dur.astype(np.int64) * dem[:, k]).sum()) // int(cap[k]))
+                 for k in range(m) if cap[k] > 0] + [0])
+    hdr[:14] = [0x52435053, n, m, int(ka.horizon), len(ka.pred_dat), W, lb,
                 max(1, top), critical_path_length(inst), off, len(levels),
-                int(int(dur.max()) > 32 or fan > 32), int(cap.sum())]
+                int(int(dur.max()) > 32 or fan > 32), int(cap.sum()), lbres]
     return np.concatenate([hdr] + [np.asarray(p, np.int32) for p in parts])
 
 
