@@ -58,10 +58,8 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
 // move shrinks from n activity steps to the suffix.
 //   o_bst: [n] starts of the current schedule; base_cmax: its makespan
 //   o_ctr: shared move counter (zeroed by the caller)
-//   per-warp scratch: tau (H+1+TAU_PAD)*W | fin [n] uint16 | log [2n] (BIG only) |
-//   ord [n + 1] uint16 (ord[n]: a valid pad the unrolled loop's prefetch may read)
-//   (16-bit finish times and activity ids: horizons and n are < 2^16, and the
-//   per-warp scratch -- what limits the warps of long horizons -- shrinks)
+//   per-warp scratch: tau (H+1+TAU_PAD)*W | fin [n] | log [2n] (BIG only) |
+//   ord [n + 1] (ord[n]: a valid pad the unrolled loop's prefetch may read)
 // The undo gives back the suffix bookings below hw_pre (a zero demand gives
 // back nothing): with durations <= 32 every suffix step's booking is found
 // from ord, the records and fin, 32 at once; with longer ones (BIG) a log
@@ -84,10 +82,10 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
                  a_tau = sa(ws), a_fin = sa(ws + (H + 1 + TAU_PAD) * W),
-                 a_log = (a_fin + 2 * n + 7) & ~7u, a_ord = a_log + (BIG ? 8 * n : 0);
+                 a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + (BIG ? 8 * n : 0);
   // the lane's base addresses of the profile and the predecessor lists
   const uint32_t a_tau_l = opaque(a_tau + 4 * W * lane), a_pdat_l = opaque(a_pdat + 4 * lane);
-  if (lane == 0) sts16(a_ord + 2 * n, 0u);
+  if (lane == 0) sts32(a_ord + 4 * n, 0u);
   // the profile is kept materialised: every slot from the high-water mark on
   // (and the 32-slot pad past the horizon the scan may read) holds the capacity
   // (capacity with every packed lane's guard bit set, see window_fits_ballot)
@@ -120,14 +118,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       if (rec.x > 0 && (r0 | r1) != 0) warp_commit_mat<W, BIG>(a_tau_l, hw_pre, s, rec.x, r0, r1);
       const int fin = s + rec.x;
       cm_pre = max(cm_pre, fin);
-      sts16_if(lane == 0, a_fin + 2 * act, static_cast<uint32_t>(fin));
+      sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
       __syncwarp();
     }
     // ---- the swapped order's suffix u.. (materialised); fin of the prefix
     // activities holds their current finish times, the suffix overwrites its
     // own entries before any successor pulls them
     for (int q = u + lane; q < n; q += 32)
-      sts16(a_ord + 2 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
+      sts32(a_ord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
     __syncwarp();
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
     bool div = false;
@@ -148,13 +146,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     // (converged: the rest is the current schedule)
     // (unrolled by two like phase B, so the prefetched activity needs no
     // register copies; p + 1 <= v + 1 < n)
-    int act = static_cast<int>(lds16(a_ord + 2 * u));
+    int act = static_cast<int>(lds32(a_ord + 4 * u));
     int4 rec = lds128(a_info + 16 * act);
     {
       int act_a = act;
       int4 rec_a = rec;
       for (;;) {
-        const int act_b = static_cast<int>(lds16(a_ord + 2 * (p + 1)));
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
                                                      hi, H, a_tau_l, a_fin, hw, cm, err);
@@ -167,7 +165,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
           break;
         }
         __syncwarp();  // after the loop test: the next REDUX follows it branch-free
-        act_a = static_cast<int>(lds16(a_ord + 2 * (p + 1)));
+        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
                                                  a_tau_l, a_fin, hw, cm, err);
@@ -190,13 +188,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       int4 rec_a = rec;
       // two steps (positions p, p + 1), the next activity prefetched
       auto pair = [&]() {
-        const int act_b = static_cast<int>(lds16(a_ord + 2 * (p + 1)));
+        const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
         int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
                                                      hi, H, a_tau_l, a_fin, hw, cm, err);
         log_below(act_a, rec_a, st);
         __syncwarp();
-        act_a = static_cast<int>(lds16(a_ord + 2 * (p + 2)));  // ord[n]: pad
+        act_a = static_cast<int>(lds32(a_ord + 4 * (p + 2)));  // ord[n]: pad
         rec_a = lds128(a_info + 16 * act_a);
         st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
                                                  a_tau_l, a_fin, hw, cm, err);
@@ -231,9 +229,9 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       // (position u + k's booking: start = fin - dur of its activity)
       for (int k0 = 0; k0 < nlog; k0 += 32) {
         const int k = k0 + lane;
-        const int a = static_cast<int>(lds16(a_ord + 2 * (u + min(k, nlog - 1))));
+        const int a = static_cast<int>(lds32(a_ord + 4 * (u + min(k, nlog - 1))));
         const int4 r = lds128(a_info + 16 * a);
-        const int f = static_cast<int>(lds16(a_fin + 2 * a));
+        const int f = static_cast<int>(lds32(a_fin + 4 * a));
         uint32_t r0 = static_cast<uint32_t>(r.y), r1 = 0u;
         if (W == 2) r1 = lds32(a_req + 8 * a + 4);
         const int s = f - r.x;

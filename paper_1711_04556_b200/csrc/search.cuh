@@ -159,8 +159,7 @@ constexpr int SNAP_MAX_BYTES = 40 * 1024;
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes, int big = 1,
                                                bool snap = false) {
-  // TIME group 32: profile | fin uint16 [n] | log [2n] (big) | ord uint16 [n+1]
-  if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 2 * n : 0) + n + 6 : (32 / G) * ((H + 1) * W + 2 * n);
+  if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return m * cap_row_stride(rmax) + n;  // c | fin (snapshots: CTA-wide)
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));

@@ -81,10 +81,6 @@ __device__ __forceinline__ void sts64_if(bool p, uint32_t a, uint32_t x, uint32_
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
 }
-__device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u16 [%1], %2;\n\t}"
-               ::"r"(static_cast<uint32_t>(p)), "r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
-}
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -332,15 +328,13 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   // loads, lanes past the span are masked (MAT: a_pdat is the lane's base)
   // (MAT: the span's start as one PRMT, then one multiply-add for the address)
   const uint32_t p0b = MAT ? __byte_perm(static_cast<uint32_t>(rec.z), 0u, 0x4410) : 0u;
-  // MAT (the prefix-reusing evaluator): fin[] holds 16-bit finish times
-  const uint32_t pidx = lds32(MAT ? a_pdat + 4 * p0b : a_pdat + 4 * (p0 + lane));
-  int f = static_cast<int>(MAT ? lds16(a_fin + 2 * pidx) : lds32(a_fin + 4 * pidx));
+  int f = static_cast<int>(lds32(a_fin + 4 * lds32(MAT ? a_pdat + 4 * p0b : a_pdat + 4 * (p0 + lane))));
   // lane < pc, as one compare of the record word with (lane + 1) << 16
   f = (MAT ? static_cast<uint32_t>(rec.z) >= ((lane + 1u) << 16) : lane < pc) ? f : 0;
   if (BIG && pc > 32)
     for (int e = lane + 32; e < pc; e += 32)
-      f = max(f, static_cast<int>(MAT ? lds16(a_fin + 2 * lds32(a_pdat + 4 * (p0 + e - lane)))
-                                      : lds32(a_fin + 4 * lds32(a_pdat + 4 * (p0 + e)))));
+      f = max(f, static_cast<int>(lds32(a_fin + 4 * lds32(MAT ? a_pdat + 4 * (p0 + e - lane)
+                                                              : a_pdat + 4 * (p0 + e)))));
   const int esv = __reduce_max_sync(FULL_MASK, f);
   const int dur = rec.x;
   const uint32_t r0 = static_cast<uint32_t>(rec.y);
@@ -366,10 +360,7 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   }
   const int fin = start + dur;
   cmax = max(cmax, fin);
-  if (MAT)
-    sts16_if(lane == 0, a_fin + 2 * act, static_cast<uint32_t>(fin));
-  else
-    sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
+  sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
   // SYNC = false: the caller synchronises after its own bookkeeping, so the
   // next step's REDUX needs no divergence check
   if (SYNC) __syncwarp();
