@@ -714,8 +714,8 @@ __device__ void import_peer_elite(const RcpspSolveArgs& A, CtaCtx& c, int iid, i
 // so the batch finishes together; without it (the reference's fixed
 // worker-to-pool mapping, and exact B = 1 trajectories) it exits.
 template <int MODE, int G, int W>
-__global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
-                                                  int n_ids, SmemPlan plan) {
+__device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restrict__ ids, int n_ids,
+                                           const SmemPlan& plan) {
   int* smem = dsm;
   const int B = static_cast<int>(A.workers);
   // with clusters (A.cluster > 1, TIME group 32 only) a worker is a cluster
@@ -972,6 +972,22 @@ __global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolve
     st[WK_T1] = static_cast<long long>(globaltimer());
     rng.store(A.w_rng + wid * 6);
   }
+}
+
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
+                                                  int n_ids, SmemPlan plan) {
+  solve_body<MODE, G, W>(A, ids, n_ids, plan);
+}
+
+// One CTA per SM with up to 32 warps (64 registers), for launches whose
+// shared memory leaves two CTAs per SM fewer warps -- 300 activities: TIME
+// ran 16 warps per SM in one 512-thread CTA (the per-warp resource profile
+// spans the horizon), CAPACITY 2 x 13.
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(1024, 1) k_solve_wide(RcpspSolveArgs A, const int* __restrict__ ids,
+                                                        int n_ids, SmemPlan plan) {
+  solve_body<MODE, G, W>(A, ids, n_ids, plan);
 }
 
 // =========================================================================
@@ -1347,6 +1363,32 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.sumcap_max)))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
+    // the wide variant (one CTA per SM, up to 32 warps at 64 registers) when
+    // it holds more warps per SM than the plan above (shared-memory-limited
+    // plans: 300 activities, both modes)
+    if constexpr (G == 32) {
+      const bool one_cta = static_cast<size_t>(p.total) * 4 > smem_per_sm() / 2 - 1024;
+      const int resident = one_cta ? nt : 2 * nt;  // resident threads per SM
+#ifndef NO_WIDE_CTA
+      if (threads == 0 && A.n_max > 64 && resident < 1024) {
+#else
+      if (false) {
+#endif
+        SmemPlan pw;
+        int ntw;
+        if (fit_plan_limit(MODE, G, static_cast<int>(A.words), static_cast<int>(A.n_max),
+                           static_cast<int>(A.m_max), static_cast<int>(A.h_max),
+                           static_cast<int>(A.e_max), static_cast<int>(A.rmax_max),
+                           static_cast<int>(A.delta), static_cast<int>(A.tabu_size), 1024,
+                           smem_optin(), 32, pw, ntw, A.no_big ? 0 : 1,
+                           static_cast<int>(A.sumcap_max)) &&
+            ntw > resident) {
+          p = pw;
+          nt = ntw;
+          k = k_solve_wide<MODE, G, W>;
+        }
+      }
+    }
     if (set_smem(k, p.total * 4)) return -1;
     // clusters need a move counter to share: the prefix-reusing evaluators
     // (TIME group 32, CAPACITY group 32, CAPACITY group 1 from 48 activities)
