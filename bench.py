@@ -74,6 +74,9 @@ def parse():
                     help="CAPACITY evaluator: 32 = warp, 1 = thread per schedule (default auto)")
     ap.add_argument("--full-sgs", action="store_true",
                     help="evaluate every swap by a full SGS (no prefix reuse)")
+    ap.add_argument("--profile-slots", type=int, default=None,
+                    help="TIME per-warp profile slots: default sized by a makespan bound when "
+                         "that keeps more warps resident; 0 = always the horizon")
     ap.add_argument("--no-steal", action="store_true",
                     help="fixed worker-to-instance mapping (no tail balancing)")
     ap.add_argument("--cpu-sample", type=int, default=None,
@@ -431,7 +434,7 @@ def main() -> None:
                       tabu_size=p.tabu_size, delta=p.delta, phi_steps=p.phi_steps,
                       phi_max=p.phi_max, seed=p.seed, group=args.group, threads=args.threads,
                       steal=not args.no_steal, full_sgs=args.full_sgs,
-                      cap_group=args.cap_group)
+                      cap_group=args.cap_group, profile_slots=args.profile_slots)
     solver = BatchSolver(insts, modes, cfg)
     solver.upload()
     stream = torch.cuda.current_stream()

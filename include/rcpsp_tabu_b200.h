@@ -109,6 +109,12 @@ typedef struct RcpspSolveArgs {
                                  * capacities (RcpspShape.sumcap): sizes the
                                  * CAPACITY evaluator's state snapshots (0 =
                                  * no snapshots, no convergence exit) */
+    int64_t prof_slots;         /* TIME: per-warp profile slots sized by a
+                                 * makespan bound (0 = the horizon); used when
+                                 * it keeps more warps resident and no_big
+                                 * holds -- a move that books past it is
+                                 * evaluated exactly on a full-horizon
+                                 * region instead */
     int32_t *ent_lock;          /* [I*F] per-entry locks (zeroed; ABI 8): the
                                  * exchange locks one entry at a time, and
                                  * ws_lock guards only the global best */

@@ -52,7 +52,7 @@ class RcpspSolveArgs(ctypes.Structure):
         ("threads", ctypes.c_int64), ("steal", ctypes.c_int64), ("full_sgs", ctypes.c_int64),
         ("cluster", ctypes.c_int64), ("time_budget_ns", ctypes.c_int64), ("t0_ns", _vp),
         ("no_big", ctypes.c_int64),
-        ("sumcap_max", ctypes.c_int64), ("ent_lock", _vp), ("outbox", _vp), ("peers", _vp), ("n_peers", ctypes.c_int64), ("peer_seen", _vp),
+        ("sumcap_max", ctypes.c_int64), ("prof_slots", ctypes.c_int64), ("ent_lock", _vp), ("outbox", _vp), ("peers", _vp), ("n_peers", ctypes.c_int64), ("peer_seen", _vp),
         ("poll_every", ctypes.c_int64), ("peer_stats", _vp),
     ]
 

@@ -10,7 +10,7 @@ namespace rt {
 enum Scal {
   SC_NFEAS = 0, SC_KEYA, SC_KEYL, SC_CUR, SC_LBEST, SC_HEAD, SC_START, SC_FLAG, SC_TOTAL,
   SC_PICKU, SC_PICKV, SC_GRANT, SC_BESTK, SC_ADOPT, SC_ENTRY, SC_DIV, SC_NONE, SC_BASEC,
-  SC_CTR, SC_STEPS, SC_BSTOK, SC_CMD, SC_NF, SC_IID, SC_PEERC, SC_PEERW, SC_WORDS = 32
+  SC_CTR, SC_STEPS, SC_BSTOK, SC_CMD, SC_NF, SC_IID, SC_PEERC, SC_PEERW, SC_FBLOCK, SC_WORDS = 32
 };
 
 struct CtaCtx {
@@ -32,6 +32,9 @@ struct CtaCtx {
   int* snap;       // CAPACITY group 32: uint16 [n/k][S] state after every k-th
                    // position of the current schedule (move starts, convergence)
   int snap_words;  // its capacity (32-bit words)
+  int* fb;         // TIME group 32 with sized per-warp profiles: the full-horizon
+                   // region for whole schedules (base pass, abandoned moves), or null
+  int slots;       // TIME group 32: profile slots per warp
   int snap_k, snap_S;  // this instance's stride k and state size S
   int warp_words;  // evaluation scratch words per warp
   int cap_lanes;   // CAP: lanes per warp that evaluate (scratch stride)

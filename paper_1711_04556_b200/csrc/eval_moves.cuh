@@ -67,21 +67,28 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
 // (W = 2)) -- and the warp gives them back one by one.
 //   ctr_cl: != 0 -> the move counter (and the step counter after it) live in
 //   the cluster leader's shared memory at this shared::cluster address
-template <int W, bool BIG>
+//   SIZED: the profile holds P slots (< H + 1 + TAU_PAD, sized by a makespan
+//   bound; no duration above 32): a move whose schedule would book past
+//   P - 64 is abandoned (time_step_pull sets ovf), the profile is rebuilt from
+//   the prefix, and the move is evaluated exactly by the full-horizon SGS on
+//   the CTA's fallback region o_fb (one warp at a time, lock at o_fblock);
+//   o_info_f / o_push: the push records and successor lists it needs.
+template <int W, bool BIG, bool SIZED>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
                                                    uint32_t cap1, uint32_t hi, int n, int H,
                                                    const uint32_t* __restrict__ moves,
                                                    int* __restrict__ cmax_out, int n_feas,
                                                    int warp_words, int base_cmax, int* err,
-                                                   uint32_t ctr_cl) {
+                                                   uint32_t ctr_cl, int P, int o_fb, int o_fblock,
+                                                   int o_info_f, int o_push) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* ws = dsm + o_evs + warp * warp_words;
   // o_info: pull records (info_r: duration, demand, predecessor span, mask);
   // o_pull: predecessor lists (pdat)
   const uint32_t a_info = sa(dsm + o_info), a_pdat = sa(dsm + o_pull), a_req = sa(dsm + o_req),
                  a_base = sa(dsm + o_base), a_bst = sa(dsm + o_bst), a_ctr = sa(dsm + o_ctr),
-                 a_tau = sa(ws), a_fin = sa(ws + (H + 1 + TAU_PAD) * W),
+                 a_tau = sa(ws), a_fin = sa(ws + P * W),
                  a_log = (a_fin + 4 * n + 7) & ~7u, a_ord = a_log + (BIG ? 8 * n : 0);
   // the lane's base addresses of the profile and the predecessor lists
   const uint32_t a_tau_l = opaque(a_tau + 4 * W * lane), a_pdat_l = opaque(a_pdat + 4 * lane);
@@ -90,10 +97,13 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   // (and the 32-slot pad past the horizon the scan may read) holds the capacity
   // (capacity with every packed lane's guard bit set, see window_fits_ballot)
   const uint32_t capg0 = cap0 | hi, capg1 = cap1 | hi;
-  for (int t = lane; t < H + 1 + TAU_PAD; t += 32) {
-    sts32(a_tau + 4 * W * t, capg0);
-    if (W == 2) sts32(a_tau + 4 * W * t + 4, capg1);
-  }
+  auto materialise = [&]() {
+    for (int t = lane; t < P; t += 32) {
+      sts32(a_tau + 4 * W * t, capg0);
+      if (W == 2) sts32(a_tau + 4 * W * t + 4, capg1);
+    }
+  };
+  materialise();
   __syncwarp();
   int up = 0, hw_pre = 0, cm_pre = 0, steps = 0;
   // the last position holds the sink (every activity precedes it, and moves
@@ -101,6 +111,26 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   // cannot change the makespan and is not scheduled
   const int pend = lds128(a_info + 16 * static_cast<int>(lds32(a_base + 4 * (n - 1)))).x == 0
                        ? n - 1 : n;
+  // SIZED: the exact makespan of the swapped order by the full-horizon SGS
+  // on the CTA's fallback region (one warp at a time)
+  auto full_eval = [&](int u, int v) -> int {
+    const uint32_t a_fb = sa(dsm + o_fb), a_fbes = a_fb + 4 * (H + 1) * W, a_fbord = a_fbes + 4 * n;
+    if (lane == 0)
+      while (atomicCAS(&dsm[o_fblock], 0, 1) != 0) __nanosleep(32);
+    __syncwarp();
+    for (int q = lane; q < n; q += 32)
+      sts32(a_fbord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
+    __syncwarp();
+    const int cmf = sgs_time_warp<W>(sa(dsm + o_info_f), sa(dsm + o_push), a_req, cap0, cap1, hi,
+                                      n, H, a_fb, a_fbes, a_fbord, nullptr, err);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) atomicExch(&dsm[o_fblock], 0);
+    return cmf;
+  };
+  // SIZED: the current schedule itself books past the profile (rare): every
+  // move of this phase is evaluated on the fallback region
+  const bool all_full = SIZED && base_cmax + 64 > P;
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = ctr_cl ? atom_add_cluster(ctr_cl, 1) : atom_inc_shared(a_ctr);
@@ -108,6 +138,12 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
     if (idx >= n_feas) break;
     const uint32_t mv = moves[idx];
     const int u = static_cast<int>(mv >> 16), v = static_cast<int>(mv & 0xffff);
+    if (SIZED && all_full) {
+      const int cmf = full_eval(u, v);
+      if (lane == 0) cmax_out[idx] = cmf;
+      steps += n;
+      continue;
+    }
     // ---- extend the prefix to positions < u with the known starts
     for (; up < u; ++up) {
       const int act = static_cast<int>(lds32(a_base + 4 * up));
@@ -128,7 +164,7 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       sts32(a_ord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));
     __syncwarp();
     int hw = hw_pre, cm = cm_pre, p = u, nlog = 0;
-    bool div = false;
+    bool div = false, ovf = false;
     // BIG: log the bookings below hw_pre for the undo (entry: dur << 16 |
     // start, demand or activity; horizons are < 2^16, see KEY_LIMIT).  !BIG
     // logs nothing: the undo finds every suffix step's booking from the
@@ -154,8 +190,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       for (;;) {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
-                                                     hi, H, a_tau_l, a_fin, hw, cm, err);
+        int st = time_step_pull<W, BIG, false, true, SIZED>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
+                                                     hi, H, a_tau_l, a_fin, hw, cm, err, P, &ovf);
         log_below(act_a, rec_a, st);
         div = st != static_cast<int>(lds32(a_bst + 4 * act_a));
         ++p;
@@ -167,8 +203,8 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
         __syncwarp();  // after the loop test: the next REDUX follows it branch-free
         act_a = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
-                                                 a_tau_l, a_fin, hw, cm, err);
+        st = time_step_pull<W, BIG, false, true, SIZED>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
+                                                 a_tau_l, a_fin, hw, cm, err, P, &ovf);
         log_below(act_b, rec_b, st);
         div = st != static_cast<int>(lds32(a_bst + 4 * act_b));
         ++p;
@@ -190,31 +226,52 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       auto pair = [&]() {
         const int act_b = static_cast<int>(lds32(a_ord + 4 * (p + 1)));
         const int4 rec_b = lds128(a_info + 16 * act_b);
-        int st = time_step_pull<W, BIG, false, true>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
-                                                     hi, H, a_tau_l, a_fin, hw, cm, err);
+        int st = time_step_pull<W, BIG, false, true, SIZED>(act_a, rec_a, a_pdat_l, a_req, cap0, cap1,
+                                                     hi, H, a_tau_l, a_fin, hw, cm, err, P, &ovf);
         log_below(act_a, rec_a, st);
         __syncwarp();
         act_a = static_cast<int>(lds32(a_ord + 4 * (p + 2)));  // ord[n]: pad
         rec_a = lds128(a_info + 16 * act_a);
-        st = time_step_pull<W, BIG, false, true>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
-                                                 a_tau_l, a_fin, hw, cm, err);
+        st = time_step_pull<W, BIG, false, true, SIZED>(act_b, rec_b, a_pdat_l, a_req, cap0, cap1, hi, H,
+                                                 a_tau_l, a_fin, hw, cm, err, P, &ovf);
         log_below(act_b, rec_b, st);
         __syncwarp();
         p += 2;
       };
       // one loop test per four positions (branches cost more than their
       // instructions here), then a pair and a single step for the rest
-      while (p + 3 < pend) {
+      while (p + 3 < pend && !(SIZED && ovf)) {
         pair();
         pair();
       }
-      if (p + 1 < pend) pair();
-      if (p < pend) {
-        const int st = time_step_pull<W, BIG, false, true>(
-            act_a, rec_a, a_pdat_l, a_req, cap0, cap1, hi, H, a_tau_l, a_fin, hw, cm, err);
+      if (p + 1 < pend && !(SIZED && ovf)) pair();
+      if (p < pend && !(SIZED && ovf)) {
+        const int st = time_step_pull<W, BIG, false, true, SIZED>(
+            act_a, rec_a, a_pdat_l, a_req, cap0, cap1, hi, H, a_tau_l, a_fin, hw, cm, err, P, &ovf);
         log_below(act_a, rec_a, st);
         ++p;
       }
+    }
+    if (SIZED && ovf) {
+      // abandoned: rebuild the profile from the prefix (whatever the suffix
+      // booked is gone with it), then the exact evaluation on the fallback
+      __syncwarp();
+      materialise();
+      __syncwarp();
+      hw_pre = 0;
+      for (int q = 0; q < up; ++q) {
+        const int act = static_cast<int>(lds32(a_base + 4 * q));
+        const int4 rec = lds128(a_info + 16 * act);
+        const uint32_t r0 = static_cast<uint32_t>(rec.y);
+        const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
+        warp_commit_mat<W, BIG>(a_tau_l, hw_pre, static_cast<int>(lds32(a_bst + 4 * act)), rec.x,
+                                r0, r1);
+        __syncwarp();
+      }
+      const int cmf = full_eval(u, v);
+      if (lane == 0) cmax_out[idx] = cmf;
+      steps += p - u + n;
+      continue;
     }
     if (lane == 0) cmax_out[idx] = div ? cm : (base_cmax | CONV_FLAG);
     steps += p - u;  // converged: p = v + 1; else pend
@@ -566,18 +623,25 @@ __device__ __forceinline__ uint32_t cluster_counter(const CtaCtx& c) {
 template <int W>
 __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int n_feas,
                                                            int base_cmax, uint32_t ctr_cl) {
+  const int full = c.I.H + 1 + TAU_PAD;
   if (c.I.big)
-    eval_moves_time32_inc<W, true>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
-                                   soff(c.base), soff(c.bst), soff(c.scal + SC_CTR), soff(c.evs),
-                                   c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H,
-                                   c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax,
-                                   c.err, ctr_cl);
+    eval_moves_time32_inc<W, true, false>(
+        soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req), soff(c.base), soff(c.bst),
+        soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+        c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax, c.err, ctr_cl,
+        full, 0, 0, 0, 0);
+  else if (c.fb && c.slots < full)
+    eval_moves_time32_inc<W, false, true>(
+        soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req), soff(c.base), soff(c.bst),
+        soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+        c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax, c.err, ctr_cl,
+        c.slots, soff(c.fb), soff(c.scal + SC_FBLOCK), soff(c.I.info_f), soff(c.I.sdat));
   else
-    eval_moves_time32_inc<W, false>(soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req),
-                                    soff(c.base), soff(c.bst), soff(c.scal + SC_CTR),
-                                    soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
-                                    c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words,
-                                    base_cmax, c.err, ctr_cl);
+    eval_moves_time32_inc<W, false, false>(
+        soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req), soff(c.base), soff(c.bst),
+        soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+        c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax, c.err, ctr_cl,
+        full, 0, 0, 0, 0);
 }
 
 // the prefix-reusing CAPACITY warp evaluator on this CTA's copy of the current order
@@ -661,8 +725,10 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
         if (warp == 0) {
           const bool keep = c.scal[SC_BSTOK] != 0;  // picked move had converged
           if (!keep) {
-            uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
-            int* es = c.evs + (c.I.H + 1) * W;
+            // (a sized per-warp profile cannot hold a whole schedule: the
+            // fallback region can)
+            uint32_t* tau = reinterpret_cast<uint32_t*>(c.fb ? c.fb : c.evs);
+            int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
             const int cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req),
                                             c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
                                             c.I.n, c.I.H, sa(tau), sa(es), sa(c.base), c.bst,
@@ -747,7 +813,7 @@ __device__ __forceinline__ int cta_eval_one(CtaCtx& c, const int* ord) {
   if (warp == 0) {
     int cm;
     if constexpr (MODE == MODE_TIME) {
-      uint32_t* tau = reinterpret_cast<uint32_t*>(c.evs);
+      uint32_t* tau = reinterpret_cast<uint32_t*>(c.fb ? c.fb : c.evs);
       int* es = reinterpret_cast<int*>(tau) + (c.I.H + 1) * W;
       cm = sgs_time_warp<W>(sa(c.I.info_f), sa(c.I.sdat), sa(c.I.req), c.I.capw[0],
                             W == 2 ? c.I.capw[1] : 0u, c.I.hi, c.I.n, c.I.H, sa(tau), sa(es),

@@ -1096,10 +1096,11 @@ size_t smem_per_sm() {
 // memory fits `limit` bytes
 bool fit_plan_limit(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
                     int T, int want_threads, size_t limit, int min_threads, SmemPlan& p,
-                    int& threads, int big = 1, int sumcap = 0) {
+                    int& threads, int big = 1, int sumcap = 0, int slots = 0) {
   for (threads = want_threads; threads >= min_threads; threads -= 32) {
     for (int lanes = 32; lanes >= (mode == MODE_CAPACITY && G == 1 ? 1 : 32); --lanes) {
-      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes, big, sumcap);
+      p = plan_smem(mode, G, W, n, m, H, e, rmax, delta, T, threads / 32, lanes, big, sumcap,
+                    slots);
       if (static_cast<size_t>(p.total) * 4 <= limit) return true;
     }
   }
@@ -1125,7 +1126,7 @@ int sm_count() {
 // threads per SM, j60: 354 M vs 311 M; j120: 2 x 512 stays best)
 bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rmax, int delta,
                      int T, int want_threads, SmemPlan& p, int& threads, long long grid = 0,
-                     int big = 1, int sumcap = 0) {
+                     int big = 1, int sumcap = 0, int slots = 0) {
   if (want_threads == 0 && n <= 64 && grid > 0) {
     const long long sms = sm_count();
     for (int per_sm : {8, 4}) {
@@ -1133,19 +1134,19 @@ bool fit_search_plan(int mode, int G, int W, int n, int m, int H, int e, int rma
       const int nt = 1024 / per_sm;
       const size_t lim = smem_per_sm() / per_sm - 1024;
       if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, nt, lim, nt, p, threads, big,
-                         sumcap))
+                         sumcap, slots))
         return true;
     }
   }
   if (want_threads == 0) {
     const size_t half = smem_per_sm() / 2 - 1024;
     if (fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, ksolve_threads(mode, G), half,
-                       256, p, threads, big, sumcap))
+                       256, p, threads, big, sumcap, slots))
       return true;
     want_threads = 512;
   }
   return fit_plan_limit(mode, G, W, n, m, H, e, rmax, delta, T, want_threads, smem_optin(), 32, p,
-                        threads, big, sumcap);
+                        threads, big, sumcap, slots);
 }
 
 template <class Kern>
@@ -1363,30 +1364,57 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.sumcap_max)))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
-    // the wide variant (one CTA per SM, up to 32 warps at 64 registers) when
-    // it holds more warps per SM than the plan above (shared-memory-limited
-    // plans: 300 activities, both modes)
+    // Alternatives when the plan above is shared-memory-limited, the one that
+    // keeps the most threads resident per SM wins (ties: the plan above):
+    //  * the wide variant (one CTA per SM, up to 32 warps at 64 registers);
+    //  * TIME: per-warp profiles sized by a makespan bound (A.prof_slots, no
+    //    duration above 32; see eval_moves_time32_inc SIZED), two CTAs or wide.
     if constexpr (G == 32) {
-      const bool one_cta = static_cast<size_t>(p.total) * 4 > smem_per_sm() / 2 - 1024;
-      const int resident = one_cta ? nt : 2 * nt;  // resident threads per SM
+      auto resident_of = [&](const SmemPlan& q, int t) {
+        return static_cast<size_t>(q.total) * 4 > smem_per_sm() / 2 - 1024 ? t : 2 * t;
+      };
+      int best = resident_of(p, nt);
+      SmemPlan q_forced;
+      int tf;
+      const int W_ = static_cast<int>(A.words), n_ = static_cast<int>(A.n_max),
+                m_ = static_cast<int>(A.m_max), H_ = static_cast<int>(A.h_max),
+                e_ = static_cast<int>(A.e_max), r_ = static_cast<int>(A.rmax_max),
+                d_ = static_cast<int>(A.delta), T_ = static_cast<int>(A.tabu_size),
+                big_ = A.no_big ? 0 : 1, sc_ = static_cast<int>(A.sumcap_max);
 #ifndef NO_WIDE_CTA
-      if (threads == 0 && A.n_max > 64 && resident < 1024) {
+      const bool try_alt = threads == 0 && A.n_max > 64 && best < 1024 && A.prof_slots >= 0;
 #else
-      if (false) {
+      const bool try_alt = false;
 #endif
-        SmemPlan pw;
-        int ntw;
-        if (fit_plan_limit(MODE, G, static_cast<int>(A.words), static_cast<int>(A.n_max),
-                           static_cast<int>(A.m_max), static_cast<int>(A.h_max),
-                           static_cast<int>(A.e_max), static_cast<int>(A.rmax_max),
-                           static_cast<int>(A.delta), static_cast<int>(A.tabu_size), 1024,
-                           smem_optin(), 32, pw, ntw, A.no_big ? 0 : 1,
-                           static_cast<int>(A.sumcap_max)) &&
-            ntw > resident) {
-          p = pw;
-          nt = ntw;
-          k = k_solve_wide<MODE, G, W>;
-        }
+      const bool try_sized = try_alt && MODE == MODE_TIME && A.no_big && A.prof_slots > 0 &&
+                             A.prof_slots < A.h_max + 1 + TAU_PAD;
+      // prof_slots < 0: sized profiles of -prof_slots slots forced (tests)
+      if (MODE == MODE_TIME && A.no_big && A.prof_slots < 0) {
+        if (!fit_search_plan(MODE, G, W_, n_, m_, H_, e_, r_, d_, T_, threads, q_forced, tf,
+                             static_cast<long long>(n_ids) * A.workers, big_, sc_,
+                             static_cast<int>(-A.prof_slots)))
+          return fail("search state does not fit in shared memory (forced profile slots)");
+        p = q_forced;
+        nt = tf;
+      }
+      SmemPlan q;
+      int tq;
+      if (try_alt && fit_plan_limit(MODE, G, W_, n_, m_, H_, e_, r_, d_, T_, 1024, smem_optin(),
+                                    32, q, tq, big_, sc_) &&
+          tq > best) {
+        p = q; nt = tq; best = tq; k = k_solve_wide<MODE, G, W>;
+      }
+      const int sl = static_cast<int>(A.prof_slots);
+      if (try_sized &&
+          fit_search_plan(MODE, G, W_, n_, m_, H_, e_, r_, d_, T_, 0, q, tq,
+                          static_cast<long long>(n_ids) * A.workers, big_, sc_, sl) &&
+          resident_of(q, tq) > best) {
+        p = q; nt = tq; best = resident_of(q, tq); k = k_solve<MODE, G, W>;
+      }
+      if (try_sized && fit_plan_limit(MODE, G, W_, n_, m_, H_, e_, r_, d_, T_, 1024,
+                                      smem_optin(), 32, q, tq, big_, sc_, sl) &&
+          tq > best) {
+        p = q; nt = tq; best = tq; k = k_solve_wide<MODE, G, W>;
       }
     }
     if (set_smem(k, p.total * 4)) return -1;

@@ -147,6 +147,8 @@ struct SmemPlan {
   int inst, base, pos, msp, mpp, rs, best, rowc, bst, tabu_list, tabu_cnt, red, scal, evs;
   int warp_words, total, cap_lanes;
   int snap, snap_words;  // CAPACITY group 32: state snapshots (uint16), -1 / 0 = none
+  int slots;             // TIME group 32: profile slots per warp
+  int fb;                // TIME group 32 with sized profiles: full-horizon region, -1 = none
 };
 
 // shared-memory budget of the CAPACITY evaluator's state snapshots: an
@@ -158,16 +160,22 @@ constexpr int SNAP_MAX_BYTES = 40 * 1024;
 // then does the prefix-reusing TIME evaluator keep an undo log (2n words)
 __host__ __device__ inline int eval_warp_words(int mode, int G, int W, int n, int m, int H,
                                                int rmax, int cap_lanes, int big = 1,
-                                               bool snap = false) {
-  if (mode == MODE_TIME) return G == 32 ? (H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3 : (32 / G) * ((H + 1) * W + 2 * n);
+                                               bool snap = false, int slots = 0) {
+  if (mode == MODE_TIME)
+    return G == 32 ? (slots > 0 ? slots : H + 1 + TAU_PAD) * W + (big ? 4 : 2) * n + 3
+                   : (32 / G) * ((H + 1) * W + 2 * n);
   if (G == 32) return m * cap_row_stride(rmax) + n;  // c | fin (snapshots: CTA-wide)
   return max(cap_lanes * cap_thread_words(n, m, rmax) + cap_prefix_words(n, m, rmax),
              cap_warp_words(n, m, rmax));
 }
 
+// slots > 0 (TIME group 32, no duration above 32): per-warp profiles of
+// that many slots plus one full-horizon region per CTA (see
+// eval_moves_time32_inc, SIZED)
 __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int m, int H, int e,
                                               int rmax, int delta, int T, int nwarps,
-                                              int cap_lanes = 32, int big = 1, int sumcap = 0) {
+                                              int cap_lanes = 32, int big = 1, int sumcap = 0,
+                                              int slots = 0) {
   SmemPlan p;
   auto a4 = [](int x) { return (x + 3) & ~3; };
   int off = 0;
@@ -195,7 +203,15 @@ __host__ __device__ inline SmemPlan plan_smem(int mode, int G, int W, int n, int
     p.snap_words = a4(static_cast<int>(need));
     off += p.snap_words;
   }
-  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big, snap));
+  const bool sized = mode == MODE_TIME && G == 32 && slots > 0 && slots < H + 1 + TAU_PAD;
+  p.slots = mode == MODE_TIME && G == 32 ? (sized ? slots : H + 1 + TAU_PAD) : 0;
+  p.fb = -1;
+  if (sized) {  // whole schedules: profile (H+1)*W | es [n] | ord [n]
+    p.fb = off;
+    off += a4((H + 1) * W + 2 * n);
+  }
+  p.warp_words = a4(eval_warp_words(mode, G, W, n, m, H, rmax, cap_lanes, big, snap,
+                                    sized ? slots : 0));
   p.evs = off; off += p.warp_words * nwarps;
   p.total = off;
   return p;
@@ -228,11 +244,14 @@ __device__ __forceinline__ void cta_setup(CtaCtx& c, const int* blob, int* smem,
   c.snap_words = p.snap_words;
   c.snap_k = 1;
   c.snap_S = 0;
+  c.fb = p.fb >= 0 ? smem + p.fb : nullptr;
+  c.slots = p.slots;
   c.warp_words = p.warp_words;
   c.cap_lanes = p.cap_lanes;
   c.moves_buf = moves_buf;
   c.cmax_buf = cmax_buf;
   c.err = err;
+  if (threadIdx.x == 0) c.scal[SC_FBLOCK] = 0;
   __syncthreads();
   if (c.snap) cta_snap_stride(c);
   cta_init_rows(c);

@@ -317,11 +317,19 @@ __device__ __forceinline__ int time_step_warp(int act, const int4& rec, uint32_t
 // activity's pull record (info_r: duration, demand, predecessor span, mask).
 // MAT: materialised profile (see window_fits_ballot); a_tau and a_pdat are
 // then the lane's base addresses (+ 4 W lane, + 4 lane).
-template <int W, bool BIG, bool SYNC = true, bool MAT = false>
+// SIZED (the search evaluator's profile of P < H + 1 + TAU_PAD slots; no
+// duration above 32): a booking must end at least 64 slots before P -- every
+// window read then stays inside the profile (a window is found in the round
+// holding max(es, hw) or the next one) -- else the step books nothing and
+// sets ovf (the caller abandons the move to an exact full-horizon
+// evaluation); with ovf already set the step touches no profile slot.
+template <int W, bool BIG, bool SYNC = true, bool MAT = false, bool SIZED = false>
 __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t a_pdat,
                                               uint32_t a_req, uint32_t cap0, uint32_t cap1,
                                               uint32_t hi, int H, uint32_t a_tau, uint32_t a_fin,
-                                              int& hw, int& cmax, int* err) {
+                                              int& hw, int& cmax, int* err, int P = 0,
+                                              bool* ovf = nullptr) {
+  static_assert(!SIZED || !BIG, "sized profiles are for durations <= 32");
   const int lane = threadIdx.x & 31;
   const int p0 = rec.z & 0xffff, pc = rec.z >> 16;
   // the predecessor lists are padded by 32 entries (common.cuh): every lane
@@ -340,7 +348,16 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
   const uint32_t r0 = static_cast<uint32_t>(rec.y);
   const uint32_t r1 = W == 2 ? lds32(a_req + 8 * act + 4) : 0u;
   int start = esv;
-  if constexpr (!BIG) {
+  if constexpr (SIZED) {
+    if (!*ovf) {
+      start = warp_window<W, BIG, false, MAT>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
+                                              static_cast<uint32_t>(rec.w), err);
+      if (start + dur + 64 > P)
+        *ovf = true;
+      else
+        warp_commit_mat<W, BIG>(a_tau, hw, start, dur, r0, r1);
+    }
+  } else if constexpr (!BIG) {
     // no branch on es < hw or on the demand: from hw on every slot is free, so
     // the first round returns es; a zero demand or duration books nothing
     start = warp_window<W, BIG, false, MAT>(a_tau, hw, H, r0, r1, cap0, cap1, hi, esv, dur,
@@ -359,7 +376,7 @@ __device__ __forceinline__ int time_step_pull(int act, const int4& rec, uint32_t
       warp_commit<W, BIG>(a_tau, hw, start, dur, r0, r1, cap0, cap1);
   }
   const int fin = start + dur;
-  cmax = max(cmax, fin);
+  if (!SIZED || !*ovf) cmax = max(cmax, fin);
   sts32_if(lane == 0, a_fin + 4 * act, static_cast<uint32_t>(fin));
   // SYNC = false: the caller synchronises after its own bookkeeping, so the
   // next step's REDUX needs no divergence check

@@ -433,6 +433,9 @@ class SolveConfig:
     cap_group: int | None = None  # CAPACITY: 32 = warp, 1 = thread per schedule, None = auto
     cluster: int | None = None    # CTAs per worker (1..8, prefix-reusing evaluators), None = auto
     time_limit_s: float | None = None  # wall-clock budget of the search on the device clock
+    # TIME: per-warp profile slots; None = sized by a makespan bound when that
+    # keeps more warps resident, 0 = always the horizon, > 0 = forced (tests)
+    profile_slots: int | None = None
 
     @property
     def block_iters(self) -> int:
@@ -492,6 +495,12 @@ class BatchSolver:
         self.rmax_max = max(int(b[B_RMAX]) for b in blobs)
         self.no_big = int(not any(int(b[B_BIG]) for b in blobs))
         self.sumcap_max = max(int(b[B_SUMCAP]) for b in blobs)
+        # TIME: per-warp profile slots sized by a makespan bound -- twice the
+        # larger of the energy and critical-path bounds plus the 64 slots a
+        # booking keeps free, plus the scan pad (the kernel uses it only when
+        # it keeps more warps resident; longer schedules fall back exactly)
+        lb = max(max(int(b[B_LBRES]), int(b[B_CPM])) for b in blobs)
+        self.prof_slots = 2 * lb + 64 + 32 + 32
         self.nbhd_max = max(1, max(neighborhood_size(int(b[B_N]), cfg.delta) for b in blobs))
         if self.nbhd_max >= KEY_LIMIT:
             raise UnsupportedInstance(f"neighbourhood of {self.nbhd_max} moves >= {KEY_LIMIT}")
@@ -605,6 +614,10 @@ class BatchSolver:
         a.time_budget_ns = int(cfg.time_limit_s * 1e9) if cfg.time_limit_s else 0
         a.no_big = self.no_big
         a.sumcap_max = self.sumcap_max
+        if cfg.profile_slots is None:
+            a.prof_slots = self.prof_slots          # auto: used when it helps
+        else:
+            a.prof_slots = -int(cfg.profile_slots)  # forced (tests), 0 = off
         a.t0_ns = ptr(self.t0)
         if self.peer is not None:
             self.peer.fill_args(a)

@@ -612,3 +612,37 @@ def test_reference_backend_fingerprint(golden):
     out["search_evals"] = stats.evaluations
     out["search_trace"] = [int(x) for chunk in stats.traces for x in chunk]
     assert json.loads(json.dumps(out)) == want
+
+
+def test_sized_profile_trajectories_match_oracle():
+    """TIME with per-warp profiles sized by a makespan bound (SolveConfig.
+    profile_slots forced): moves that would book past the profile are
+    abandoned and evaluated exactly on the CTA's full-horizon region.  B = 1
+    trajectories equal the oracle's with a generous size (overflow rare), a
+    tight one (frequent fallbacks) and one below the current schedule's
+    makespan (every move on the fallback)."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts = synth.benchmark_batch("j60p", 2, first_seed=0) + \
+        synth.benchmark_batch("j120p", 1, first_seed=3)
+    want = [oracle.orchestrate(x, 60, 1, 3, 1, delta=60, tabu_size=250, pool_size=8,
+                               collect_trace=True) for x in insts]
+    for slots in (400, 160, 96):
+        cfg = SolveConfig(total_iters=60, workers=1, pool_size=8, tabu_size=250, delta=60,
+                          phi_steps=20, phi_max=3, seed=3, collect_trace=True, cluster=1,
+                          profile_slots=slots)
+        r = BatchSolver(insts, [1] * len(insts), cfg).run()
+        for i, w in enumerate(want):
+            assert int(r.best_cmax[i]) == w["best_cmax"], (slots, i)
+            assert int(r.evaluations[i]) == w["evaluations"], (slots, i)
+            assert [t.tolist() for t in r.traces[i]] == [t.tolist() for t in w["traces"]], \
+                (slots, i)
+    # the auto choice on a 300-activity batch keeps the budget accounting and
+    # valid best schedules
+    big = synth.benchmark_batch("act300", 4, first_seed=9)
+    cfg = SolveConfig(total_iters=20, workers=2, pool_size=8, tabu_size=800, delta=60,
+                      phi_steps=20, phi_max=3, seed=1)
+    r = BatchSolver(big, [1] * 4, cfg).run()
+    for i, inst in enumerate(big):
+        assert r.iterations[i] == 20 or r.best_cmax[i] == r.critical_path[i]
+        n = inst.n_activities
+        assert evaluate(r.best_order[i, :n], inst, 1).cmax == int(r.best_cmax[i])
