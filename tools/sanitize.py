@@ -88,6 +88,18 @@ def main() -> None:
                     assert int(r.evaluations[i]) == want["evaluations"], (i, mode, cluster)
             else:
                 assert ((r.iterations == 30) | (r.best_cmax == r.critical_path)).all()
+    # TIME with makespan-bounded per-warp profiles forced tight (fallback path)
+    j60 = synth.benchmark_batch("j60p", 2, first_seed=0)
+    for slots in (160, 96):
+        cfg = SolveConfig(total_iters=15, workers=1, pool_size=4, tabu_size=60, delta=20,
+                          phi_steps=5, phi_max=1, seed=1, cluster=1, profile_slots=slots)
+        r = BatchSolver(j60, [1, 1], cfg).run()
+        for i, inst in enumerate(j60):
+            want = oracle.orchestrate(inst, 15, 1, 1, 1, delta=20, tabu_size=60, phi_steps=5,
+                                      phi_max=1, pool_size=4)
+            assert int(r.best_cmax[i]) == want["best_cmax"], ("sized", slots, i)
+            assert int(r.evaluations[i]) == want["evaluations"], ("sized", slots, i)
+    print("sized profiles ok", flush=True)
     s = BatchSolver(insts, [1] * len(insts), SolveConfig(total_iters=10, workers=1, pool_size=4,
                                                          tabu_size=30, delta=20, phi_steps=5,
                                                          phi_max=1, seed=2))
