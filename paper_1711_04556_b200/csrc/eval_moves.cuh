@@ -115,8 +115,14 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
   // on the CTA's fallback region (one warp at a time)
   auto full_eval = [&](int u, int v) -> int {
     const uint32_t a_fb = sa(dsm + o_fb), a_fbes = a_fb + 4 * (H + 1) * W, a_fbord = a_fbes + 4 * n;
-    if (lane == 0)
+    // (acquire: the fence orders the previous holder's accesses, released by
+    // its fence + exchange below, before this warp's; compute-sanitizer
+    // racecheck does not model such a lock and reports the region's reuse by
+    // the next warp as a race -- profiles/r2/sanitizer3/README.md)
+    if (lane == 0) {
       while (atomicCAS(&dsm[o_fblock], 0, 1) != 0) __nanosleep(32);
+      __threadfence_block();
+    }
     __syncwarp();
     for (int q = lane; q < n; q += 32)
       sts32(a_fbord + 4 * q, lds32(a_base + 4 * (q == u ? v : (q == v ? u : q))));

@@ -29,7 +29,7 @@ from paper_1711_04556_b200 import device  # noqa: E402
 from paper_1711_04556_b200.device import BatchSolver, SolveConfig  # noqa: E402
 
 
-def main() -> None:
+def main(sections: set[str]) -> None:
     import torch
     rng = np.random.default_rng(0)
     j30 = synth.benchmark_batch("j30p", 2, first_seed=3)
@@ -37,7 +37,7 @@ def main() -> None:
     big = synth.random_instance(20, 3, seed=77, cap_lo=4, cap_hi=9, max_dur=45,
                                 demand_density=0.8)          # durations > 32 (B_BIG)
     # K1
-    for inst in (j30[0], j60, big):
+    for inst in ((j30[0], j60, big) if "K1" in sections else ()):
         orders = np.stack([random_topological_order(inst, rng) for _ in range(9)])
         for mode, groups in ((1, (32, 16, 8)), (0, (32, 1))):
             want, _ = oracle.evaluate_batch(inst, orders, mode)
@@ -49,6 +49,8 @@ def main() -> None:
             assert device.eval_batch(inst, rev, mode, reverse=True)[0].tolist() == want_r.tolist()
     print("K1 ok", flush=True)
     # filter / diversify / state ops
+    if "misc" not in sections:
+        return _rest(sections, rng, j30, j60, big)
     o = random_topological_order(j60, rng)
     got = device.filter_batch(j60, o[None], 7)[0]
     assert got.tolist() == oracle.filter_moves(j60, o, oracle.neighborhood(j60.n_activities, 7)).tolist()
@@ -57,8 +59,13 @@ def main() -> None:
     state = np.zeros((j60.n_resources, int(j60.capacities.max())), np.int32)
     device.state_op(j60, "cap_update", state, 3, 0)
     print("filter/diversify/state ok", flush=True)
+    _rest(sections, rng, j30, j60, big)
+
+
+def _rest(sections, rng, j30, j60, big) -> None:
+    import torch
     # K2 (the operator's cluster choice spreads a batch of 1 over 8 CTAs)
-    for inst in (j30[0], big):
+    for inst in ((j30[0], big) if "K2" in sections else ()):
         orders = np.stack([random_topological_order(inst, rng) for _ in range(2)])
         cm, _ = oracle.evaluate_batch(inst, orders, 1)
         for mode, group in ((1, 32), (0, 32), (0, 1)):
@@ -74,7 +81,7 @@ def main() -> None:
     print("K2 ok", flush=True)
     # K0 + K3 + K4
     insts = j30 + [j60, big]
-    for mode, cap_group in ((1, None), (0, 32), (0, 1)):
+    for mode, cap_group in ((1, None), (0, 32), (0, 1)) if "K3" in sections else ():
         for workers, cluster in ((1, 1), (1, 2), (3, 1), (2, 4)):
             cfg = SolveConfig(total_iters=30, workers=workers, pool_size=4, tabu_size=30,
                               delta=20, phi_steps=5, phi_max=1, seed=1, cluster=cluster,
@@ -90,7 +97,7 @@ def main() -> None:
                 assert ((r.iterations == 30) | (r.best_cmax == r.critical_path)).all()
     # TIME with makespan-bounded per-warp profiles forced tight (fallback path)
     j60 = synth.benchmark_batch("j60p", 2, first_seed=0)
-    for slots in (160, 96):
+    for slots in (160, 96) if "sized" in sections else ():
         cfg = SolveConfig(total_iters=15, workers=1, pool_size=4, tabu_size=60, delta=20,
                           phi_steps=5, phi_max=1, seed=1, cluster=1, profile_slots=slots)
         r = BatchSolver(j60, [1, 1], cfg).run()
@@ -100,6 +107,8 @@ def main() -> None:
             assert int(r.best_cmax[i]) == want["best_cmax"], ("sized", slots, i)
             assert int(r.evaluations[i]) == want["evaluations"], ("sized", slots, i)
     print("sized profiles ok", flush=True)
+    if "K4" not in sections:
+        return
     s = BatchSolver(insts, [1] * len(insts), SolveConfig(total_iters=10, workers=1, pool_size=4,
                                                          tabu_size=30, delta=20, phi_steps=5,
                                                          phi_max=1, seed=2))
@@ -113,5 +122,7 @@ def main() -> None:
     print("K0/K3/K4 ok", flush=True)
 
 
+ALL = {"K1", "misc", "K2", "K3", "sized", "K4"}
+
 if __name__ == "__main__":
-    main()
+    main(set(sys.argv[1:]) or ALL)
