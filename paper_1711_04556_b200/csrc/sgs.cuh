@@ -612,7 +612,7 @@ __host__ __device__ __forceinline__ int cap_thread_words(int n, int m, int rmax)
 // Warp-cooperative capacity-indexed SGS (group 32): one warp per schedule.
 // Lane k < m holds resource k's capacity and demand, so Eq. 7's max over the
 // resources is one REDUX; Alg. 4 then runs per demanded resource with the
-// whole warp in closed form (cap_update_warp).  Rows are `rs` words apart
+// whole warp in closed form (cap_update_row).  Rows are `rs` words apart
 // (rmax rounded up to odd: the m rows fall in distinct banks).
 //   scratch: c [m*rs] | es [n]
 
@@ -644,82 +644,18 @@ __host__ __device__ __forceinline__ int cap_prefix_words(int n, int m, int rmax)
 //    their values (no stop: the shift runs to the end of the row).
 // One warp-wide inclusive scan per 32 entries finds t; the reference's loop
 // walks the row entry by entry on one thread.
-__device__ __forceinline__ void cap_update_warp(uint32_t a_row, int capk, int r, int s, int d) {
-  const int lane = threadIdx.x & 31;
-  const int T = s + d;
-  int i0 = capk, c0 = 0;
-  for (int b = 0; b < capk; b += 32) {
-    const int i = b + lane;
-    const int v = i < capk ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-    const unsigned msk = __ballot_sync(FULL_MASK, i < capk && v < T);
-    if (msk) {
-      const int l = __ffs(msk) - 1;
-      i0 = b + l;
-      c0 = __shfl_sync(FULL_MASK, v, l);
-      break;
-    }
-  }
-  if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
-  __syncwarp();
-  if (c0 <= s) {
-    for (int j = lane; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
-    __syncwarp();
-    return;
-  }
-  int carry = 0, t = capk, newt = 0, b = i0, oir = 0;
-  for (;; b += 32) {
-    const int i = b + lane;
-    const bool in = i < capk, sh = i >= i0 + r;
-    const int oi = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-    oir = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
-    const int f = max(oi, s);
-    const int g = in ? (sh ? oir - f : s - f) : 0;
-    int S = g;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL_MASK, S, o);
-      if (lane >= o) S += y;
-    }
-    S += carry;
-    const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
-    if (term) {
-      const int l = __ffs(term) - 1;
-      t = b + l;
-      newt = __shfl_sync(FULL_MASK, f - (S - g), l);
-      break;
-    }
-    if (b + 32 >= capk) break;
-    carry = __shfl_sync(FULL_MASK, S, 31);
-  }
-  const int end = t < capk ? t : capk;  // [i0, end): T / shifted; t: newt
-  __syncwarp();
-  if (b == i0) {  // one chunk: every old value is in registers
-    const int i = i0 + lane;
-    if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : oir));
-    if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
-  } else {
-    // backward over the chunks: a chunk reads c[i - r] (lower entries) before
-    // its lanes write, and no lower chunk has been written yet
-    for (int bb = b; bb >= i0; bb -= 32) {
-      const int i = bb + lane;
-      const int v = (i < end && i >= i0 + r) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : T;
-      __syncwarp();
-      if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(v));
-      if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
-      __syncwarp();
-    }
-  }
-  __syncwarp();
-}
-
-// cap_update_warp on up to K 32-entry windows starting at i0 (entry i0 +
-// 32k + lane in lane `lane` of window k): each window is read once, the
-// shifted value c[i - r] is a shuffle within window 0 for demands below 32
-// and a load otherwise, one warp-wide scan per window finds the stop t, and
-// the writes follow once every read is done.  If the surplus outlasts the K
-// windows the generic form runs instead (nothing has been written yet).
-template <int K>
-__device__ __forceinline__ void cap_update_win(uint32_t a_row, int capk, int r, int s, int d) {
+//
+// Alg. 4 on one row in windows of 32 entries aligned at i0 (entry i0 + 32k +
+// lane in lane `lane` of window k): window 0 is held in registers, its
+// shifted value c[i - r] a shuffle for demands below 32; one warp-wide scan
+// per window finds the stop t, carrying the surplus into the next window
+// (rows longer than a warp); the writes follow once every read is done --
+// the later windows backward (each reads its c[i - r] before its lanes
+// write, and no lower window has been written yet), window 0 from registers.
+// A/B on B200 (tools/ab_args.sh, profiles/r2/cap_ab.txt): three windows held
+// in registers cost spills on the common path; 384 threads per CTA to avoid
+// them: -13 %.
+__device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
   const int lane = threadIdx.x & 31;
   const int T = s + d;
   int i0 = capk, c0 = 0;
@@ -741,80 +677,90 @@ __device__ __forceinline__ void cap_update_win(uint32_t a_row, int capk, int r, 
     __syncwarp();
     return;
   }
-  int ov[K];
-  int carry = 0, t = capk, newt = 0, last = -1;
+  int t = capk, newt = 0, ov0, b = i0;
+  {  // window 0
+    const int i = i0 + lane;
+    const bool in = i < capk, sh = i >= i0 + r;
+    const int w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+    int o;
+    if (r < 32)
+      o = __shfl_sync(FULL_MASK, w, (lane - r) & 31);
+    else
+      o = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
+    ov0 = o;
+    const int f = max(w, s);
+    const int g = in ? (sh ? o - f : s - f) : 0;
+    int S = g;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (last < 0) {
-      const int i = i0 + 32 * k + lane;
-      const bool in = i < capk, sh = i >= i0 + r;
-      const int w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
-      int o;
-      if (k == 0 && r < 32)
-        o = __shfl_sync(FULL_MASK, w, (lane - r) & 31);
-      else
-        o = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
-      ov[k] = o;
-      const int f = max(w, s);
-      const int g = in ? (sh ? o - f : s - f) : 0;
-      int S = g;
+    for (int q = 1; q < 32; q <<= 1) {
+      const int y = __shfl_up_sync(FULL_MASK, S, q);
+      if (lane >= q) S += y;
+    }
+    const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
+    if (term) {
+      const int l = __ffs(term) - 1;
+      t = i0 + l;
+      newt = __shfl_sync(FULL_MASK, f - (S - g), l);
+    } else if (i0 + 32 < capk) {
+      // the surplus outlasts window 0: the next windows, carrying it
+      int carry = __shfl_sync(FULL_MASK, S, 31);
+      for (b = i0 + 32;; b += 32) {
+        const int i = b + lane;
+        const bool in = i < capk, sh = i >= i0 + r;
+        const int w = in ? static_cast<int>(lds32(a_row + 4 * i)) : 0;
+        const int o = (in && sh) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : 0;
+        const int f = max(w, s);
+        const int g = in ? (sh ? o - f : s - f) : 0;
+        int S = g;
 #pragma unroll
-      for (int q = 1; q < 32; q <<= 1) {
-        const int y = __shfl_up_sync(FULL_MASK, S, q);
-        if (lane >= q) S += y;
-      }
-      S += carry;
-      const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
-      if (term) {
-        const int l = __ffs(term) - 1;
-        t = i0 + 32 * k + l;
-        newt = __shfl_sync(FULL_MASK, f - (S - g), l);
-        last = k;
-      } else if (i0 + 32 * (k + 1) >= capk) {
-        last = k;  // no stop: the shift runs to the row's end
-      } else {
+        for (int q = 1; q < 32; q <<= 1) {
+          const int y = __shfl_up_sync(FULL_MASK, S, q);
+          if (lane >= q) S += y;
+        }
+        S += carry;
+        const unsigned term = __ballot_sync(FULL_MASK, in && sh && S >= 0);
+        if (term) {
+          const int l = __ffs(term) - 1;
+          t = b + l;
+          newt = __shfl_sync(FULL_MASK, f - (S - g), l);
+          break;
+        }
+        if (b + 32 >= capk) break;  // no stop: the shift runs to the row's end
         carry = __shfl_sync(FULL_MASK, S, 31);
       }
     }
   }
-  if (last < 0) {  // the stop lies past the windows (rare)
-    cap_update_warp(a_row, capk, r, s, d);
-    return;
-  }
+  const int end = t < capk ? t : capk;  // [i0, end): T / shifted; t: newt
   __syncwarp();
-  const int end = t < capk ? t : capk;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (k <= last) {
-      const int i = i0 + 32 * k + lane;
-      if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : ov[k]));
-      if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
-    }
+  for (int bb = b; bb > i0; bb -= 32) {  // the later windows, backward
+    const int i = bb + lane;
+    const int v = (i < end && i >= i0 + r) ? static_cast<int>(lds32(a_row + 4 * (i - r))) : T;
+    __syncwarp();
+    if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(v));
+    if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
+    __syncwarp();
   }
+  const int i = i0 + lane;
+  if (i < end) sts32(a_row + 4 * i, static_cast<uint32_t>(i < i0 + r ? T : ov0));
+  if (i == t) sts32(a_row + 4 * i, static_cast<uint32_t>(newt));
   __syncwarp();
-}
-
-// Alg. 4 on one row: one 32-entry window from i0 (demands below 32 with the
-// stop within the window -- the common case), else the generic form.  A/B on
-// B200 (tools/ab_args.sh, profiles/r2/cap_ab.txt): three windows held in
-// registers cost spills on the common path (-5 % j120p, -7 % j60p, +5 % on
-// the 300-activity set); 384 threads per CTA to avoid them: -13 %.
-__device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
-  cap_update_win<1>(a_row, capk, r, s, d);
 }
 
 // Alg. 4 for every resource the activity demands (lane k < m: capacity,
 // demand and row offset -- in words from a_c -- of resource k), one after
-// another with the whole warp.
+// another with the whole warp (capacity and demand travel in one shuffle:
+// both are below 2^16, a row fits in shared memory).
 __device__ __forceinline__ void cap_update_all(uint32_t a_c, int off, int m, int capk, int req,
                                                int start, int dur) {
   const int lane = threadIdx.x & 31;
   unsigned used = __ballot_sync(FULL_MASK, lane < m && req > 0);
+  const int cr = capk | (req << 16);
+  const uint32_t a_row = a_c + 4 * off;
   while (used) {
     const int k = __ffs(used) - 1;
     used &= used - 1;
-    cap_update_row(a_c + 4 * __shfl_sync(FULL_MASK, off, k), __shfl_sync(FULL_MASK, capk, k),
-                   __shfl_sync(FULL_MASK, req, k), start, dur);
+    const int x = __shfl_sync(FULL_MASK, cr, k);
+    cap_update_row(__shfl_sync(FULL_MASK, a_row, k), x & 0xffff, x >> 16, start, dur);
   }
 }
 

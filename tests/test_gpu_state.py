@@ -105,12 +105,12 @@ def test_state_ops_fuzz_vs_oracle():
 def test_cap_update_closed_form_random_rows():
     """Alg. 4 on arbitrary descending rows -- runs of equal entries, rows
     longer than a warp (up to 120 entries), demands above 32 -- through
-    rcpsp_state_op (the SGS's warp-wide closed form, sgs.cuh:cap_update_warp)
+    rcpsp_state_op (the SGS's warp-wide closed form, sgs.cuh:cap_update_row)
     against the reference's loop (oracle.cap_update, kernels.py:81-110).
     Starts are at or above the Eq. 7 bound, as the SGS guarantees."""
     rng = np.random.default_rng(11)
-    for trial in range(400):
-        cap = int(rng.choice([3, 17, 40, 75, 120]))
+    for trial in range(1500):
+        cap = int(rng.choice([3, 17, 33, 40, 64, 75, 120]))
         m = int(rng.integers(1, 4))
         caps = [cap] + [int(rng.integers(1, cap + 1)) for _ in range(m - 1)]
         dur = int(rng.integers(1, 13))
