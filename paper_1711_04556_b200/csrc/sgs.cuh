@@ -645,6 +645,46 @@ __host__ __device__ __forceinline__ int cap_prefix_words(int n, int m, int rmax)
 // One warp-wide inclusive scan per 32 entries finds t; the reference's loop
 // walks the row entry by entry on one thread.
 //
+// Alg. 4 on a row of at most 32 entries (most rows: capacities <= 32): the
+// row is loaded once, one entry per lane, and everything else is register
+// work -- i0 is the first lane below T; the fast case (c[i0] <= s) holds iff
+// no entry lies in (s, T) (entries before i0 are >= T, the row descends);
+// c[i - r] is a shuffle; one warp-wide scan finds the stop t; one predicated
+// store per lane writes the row.
+__device__ __forceinline__ void cap_update_short(uint32_t a_row, int capk, int r, int s, int d) {
+  const int lane = threadIdx.x & 31;
+  const int T = s + d;
+  const bool in = lane < capk;
+  const int w = in ? static_cast<int>(lds32(a_row + 4 * lane)) : 0;
+  const int i0 = __ffs(__ballot_sync(FULL_MASK, in && w < T)) - 1;  // >= 0 by Eq. 7
+  const bool mid = __any_sync(FULL_MASK, in && w > s && w < T);
+  const bool pre = lane >= i0 && lane < i0 + r;
+  if (!mid) {  // entries i0..i0+r-1 become T (i0 + r <= capk by Eq. 7)
+    __syncwarp();
+    sts32_if(pre, a_row + 4 * lane, static_cast<uint32_t>(T));
+    __syncwarp();
+    return;
+  }
+  const int o = __shfl_sync(FULL_MASK, w, (lane - r) & 31);  // c[lane - r]
+  const bool sh = in && lane >= i0 + r;
+  const int f = max(w, s);
+  const int g = pre ? s - f : (sh ? o - f : 0);
+  int S = g;
+#pragma unroll
+  for (int q = 1; q < 32; q <<= 1) {
+    const int y = __shfl_up_sync(FULL_MASK, S, q);
+    if (lane >= q) S += y;
+  }
+  const unsigned term = __ballot_sync(FULL_MASK, sh && S >= 0);
+  const int l = __ffs(term) - 1;  // -1: no stop, the shift runs to the row's end
+  const int newt = __shfl_sync(FULL_MASK, f - (S - g), l & 31);
+  const int end = term ? l : capk;
+  __syncwarp();
+  sts32_if(lane >= i0 && (lane < end || lane == l), a_row + 4 * lane,
+           static_cast<uint32_t>(lane == l ? newt : (pre ? T : o)));
+  __syncwarp();
+}
+
 // Alg. 4 on one row in windows of 32 entries aligned at i0 (entry i0 + 32k +
 // lane in lane `lane` of window k): window 0 is held in registers, its
 // shifted value c[i - r] a shuffle for demands below 32; one warp-wide scan
@@ -656,6 +696,10 @@ __host__ __device__ __forceinline__ int cap_prefix_words(int n, int m, int rmax)
 // in registers cost spills on the common path; 384 threads per CTA to avoid
 // them: -13 %.
 __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, int s, int d) {
+  if (capk <= 32) {
+    cap_update_short(a_row, capk, r, s, d);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int T = s + d;
   int i0 = capk, c0 = 0;
@@ -673,7 +717,8 @@ __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, 
   if (i0 >= capk) return;  // cannot happen: Eq. 7 gives c[capk - r] <= s < T
   if (c0 <= s) {
     __syncwarp();  // every lane's read of the row precedes the writes
-    for (int j = lane; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
+    sts32_if(lane < r, a_row + 4 * (i0 + lane), static_cast<uint32_t>(T));
+    for (int j = lane + 32; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
     __syncwarp();
     return;
   }

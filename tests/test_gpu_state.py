@@ -110,7 +110,7 @@ def test_cap_update_closed_form_random_rows():
     Starts are at or above the Eq. 7 bound, as the SGS guarantees."""
     rng = np.random.default_rng(11)
     for trial in range(1500):
-        cap = int(rng.choice([3, 17, 33, 40, 64, 75, 120]))
+        cap = int(rng.choice([3, 17, 31, 32, 33, 40, 64, 75, 120]))
         m = int(rng.integers(1, 4))
         caps = [cap] + [int(rng.integers(1, cap + 1)) for _ in range(m - 1)]
         dur = int(rng.integers(1, 13))
