@@ -194,12 +194,15 @@ def pick_cluster(workers_total: int) -> int:
 
 
 def pick_cap_group(n: int, m: int, rmax: int) -> int:
-    """CAPACITY evaluator for the search kernel (measured on B200,
-    profiles/r1/configs): one thread per schedule while its per-thread state
-    (m*rmax + rmax + n words) is small -- j30/j60/j120: 1.45x/1.5x/1.07x the
-    warp evaluator -- else one warp per schedule (300 activities, capacity 80:
-    the per-thread state leaves too few lanes resident)."""
-    return 1 if m * rmax + rmax + n <= 256 else 32
+    """CAPACITY evaluator for the search kernel: one warp per schedule.
+    Measured on B200 (profiles/r2/cap_group.txt) once rows of up to 32
+    entries are updated in registers: the warp evaluator beats one thread per
+    schedule on every config where the thread's state is small enough to
+    compete -- Gen-R j120 99 vs 89 M schedules/s, j60 184 vs 164 M, j30 295 vs
+    236 M, Gen-P j30 169 vs 41 M (round 1 picked one thread per schedule for
+    states of <= 256 words).  `SolveConfig.cap_group = 1` still selects it."""
+    del n, m, rmax
+    return 32
 
 
 # ---------------------------------------------------------------------------
