@@ -224,12 +224,12 @@ def test_product_never_imports_oracle():
 
 
 def test_b200_rules_match_measurements():
-    """B200_RULES pick the mode the device measured faster on 11 of the 12
-    families of profiles/r1/mode_rules_b200.json (tools/derive_rules.py)."""
+    """B200_RULES pick the mode the device measured faster on every family
+    of profiles/r2/mode_rules_b200.json (tools/derive_rules.py)."""
     import json
     from types import SimpleNamespace
     from paper_1711_04556_b200 import B200_RULES, DEFAULT_RULES, EvalMode, decide_static
-    rows = json.loads((ROOT / "profiles" / "r1" / "mode_rules_b200.json").read_text())["rows"]
+    rows = json.loads((ROOT / "profiles" / "r2" / "mode_rules_b200.json").read_text())["rows"]
     hits = 0
     for r in rows:
         f = SimpleNamespace(max_capacity=r["cap"][1], avg_duration=r["avg_duration"],
@@ -237,7 +237,7 @@ def test_b200_rules_match_measurements():
                             avg_branch_factor=1.5, critical_path_length=0)
         got = decide_static(f, B200_RULES)
         hits += got == (EvalMode.CAPACITY if r["faster"] == "capacity" else EvalMode.TIME)
-    assert hits >= 11
+    assert hits == len(rows) == 15
     # the Gen-R benchmark configs keep TIME under both rule sets
     f = SimpleNamespace(max_capacity=16, avg_duration=5.5, min_capacity=10, avg_capacity=13,
                         avg_branch_factor=1.5, critical_path_length=0)

@@ -3,7 +3,8 @@
 item 3; the paper's method): time the search kernel in both
 modes on instance families that vary the two features the reference's rules
 test (max capacity, average duration) and report which mode evaluates more
-schedules per second.  Writes profiles/r1/mode_rules_b200.json.
+schedules per second.  Writes profiles/r2/mode_rules_b200.json (round 1:
+profiles/r1/).
 
 usage: python tools/derive_rules.py [--instances 148] [--iters 100]"""
 import argparse
@@ -22,12 +23,13 @@ def main():
     ap.add_argument("--instances", type=int, default=148)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=120)
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r2" / "mode_rules_b200.json"))
     args = ap.parse_args()
     import torch
     from paper_1711_04556_b200 import SearchParams, extract_features, synth
     from paper_1711_04556_b200.device import BatchSolver, SolveConfig
     rows = []
-    for cap_lo, cap_hi in ((2, 6), (4, 10), (10, 16), (40, 80)):
+    for cap_lo, cap_hi in ((2, 6), (4, 10), (10, 16), (16, 32), (40, 80)):
         for max_dur in (10, 20, 40):
             insts = [synth.random_instance(args.n, 4, seed=s, cap_lo=cap_lo, cap_hi=cap_hi,
                                            max_dur=max_dur, demand_density=0.5)
@@ -55,7 +57,7 @@ def main():
             print(f"cap {cap_lo}-{cap_hi} dur<= {max_dur}: TIME {rec['time']['sched_per_s']/1e6:8.2f} M/s "
                   f"(dev {rec['time']['cpm_dev']:6.1f}%)  CAP {rec['capacity']['sched_per_s']/1e6:8.2f} M/s "
                   f"(dev {rec['capacity']['cpm_dev']:6.1f}%)  -> {rec['faster']}", flush=True)
-    out = ROOT / "profiles" / "r1" / "mode_rules_b200.json"
+    out = Path(args.out)
     out.write_text(json.dumps({"n": args.n, "instances": args.instances, "iters": args.iters,
                                "rows": rows}, indent=1))
     print("wrote", out)
