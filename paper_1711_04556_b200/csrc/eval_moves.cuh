@@ -627,7 +627,10 @@ __device__ __forceinline__ uint32_t cluster_counter(const CtaCtx& c) {
 
 // the prefix-reusing TIME evaluator on this CTA's copy of the current order
 template <int W>
-__device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int n_feas,
+// (noinline: keeps the evaluators' argument set out of the search loop's
+// register allocation -- A/B on B200, profiles/r2/ab_dispatch_noinline.txt:
+// j30 +10 %, j30p +6 %, j60p +2 %, j120p +0.5 %, j120p CAPACITY +1.3 %)
+__device__ __noinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int n_feas,
                                                            int base_cmax, uint32_t ctr_cl) {
   const int full = c.I.H + 1 + TAU_PAD;
   if (c.I.big)
@@ -651,7 +654,7 @@ __device__ __forceinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int 
 }
 
 // the prefix-reusing CAPACITY warp evaluator on this CTA's copy of the current order
-__device__ __forceinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
+__device__ __noinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n_feas,
                                                              bool reuse, uint32_t ctr_cl,
                                                              int base_cmax) {
   if (c.I.big)
