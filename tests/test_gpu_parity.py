@@ -646,3 +646,32 @@ def test_sized_profile_trajectories_match_oracle():
         assert r.iterations[i] == 20 or r.best_cmax[i] == r.critical_path[i]
         n = inst.n_activities
         assert evaluate(r.best_order[i, :n], inst, 1).cmax == int(r.best_cmax[i])
+
+
+def test_capacity_beyond_time_packing():
+    """CAPACITY has no packing limit (kernels.py:68-110 works on any m and
+    capacity): instances with 9-24 resources, or more than 4 resources with
+    capacities above 127, evaluate and search in CAPACITY mode equal to the
+    oracle, while TIME is refused loudly (its packed profile cannot hold them)."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    rng = np.random.default_rng(29)
+    insts = [synth.random_instance(30, 12, seed=1, cap_lo=5, cap_hi=20, demand_density=0.5),
+             synth.random_instance(40, 6, seed=2, cap_lo=100, cap_hi=250, demand_density=0.6),
+             synth.random_instance(25, 24, seed=3, cap_lo=2, cap_hi=9, demand_density=0.3)]
+    for inst in insts:
+        orders = np.stack([random_topological_order(inst, rng) for _ in range(40)])
+        want_c, want_s = oracle.evaluate_batch(inst, orders, 0)
+        for g in CAP_GROUPS:
+            got_c, got_s = device.eval_batch(inst, orders, 0, group=g)
+            assert np.array_equal(got_c, want_c) and np.array_equal(got_s, want_s), inst.name
+        with pytest.raises(ValueError):
+            device.eval_batch(inst, orders, 1)
+    cfg = SolveConfig(total_iters=30, workers=1, pool_size=6, tabu_size=60, delta=30,
+                      phi_steps=20, phi_max=3, seed=3, collect_trace=True)
+    r = BatchSolver(insts, [0] * len(insts), cfg).run()
+    for i, inst in enumerate(insts):
+        want = oracle.orchestrate(inst, 30, 1, 3, 0, delta=30, tabu_size=60, pool_size=6,
+                                  collect_trace=True)
+        assert int(r.best_cmax[i]) == want["best_cmax"], i
+        assert int(r.evaluations[i]) == want["evaluations"], i
+        assert [t.tolist() for t in r.traces[i]] == [t.tolist() for t in want["traces"]], i
