@@ -112,7 +112,8 @@ typedef struct RcpspSolveArgs {
     int64_t prof_slots;         /* TIME: per-warp profile slots sized by a
                                  * makespan bound (0 = the horizon); used when
                                  * it keeps more warps resident and no_big
-                                 * holds -- a move that books past it is
+                                 * holds (< 0: -prof_slots slots, always --
+                                 * tests) -- a move that books past it is
                                  * evaluated exactly on a full-horizon
                                  * region instead */
     int32_t *ent_lock;          /* [I*F] per-entry locks (zeroed; ABI 8): the
