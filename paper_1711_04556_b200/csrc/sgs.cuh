@@ -718,7 +718,10 @@ __device__ __forceinline__ void cap_update_row(uint32_t a_row, int capk, int r, 
   if (c0 <= s) {
     __syncwarp();  // every lane's read of the row precedes the writes
     sts32_if(lane < r, a_row + 4 * (i0 + lane), static_cast<uint32_t>(T));
-    for (int j = lane + 32; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
+    if (r > 32) {  // (uniform; keeps the loop's trip-count set-up off the common path)
+#pragma unroll 1
+      for (int j = lane + 32; j < r; j += 32) sts32(a_row + 4 * (i0 + j), static_cast<uint32_t>(T));
+    }
     __syncwarp();
     return;
   }
