@@ -64,16 +64,23 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
 }
 
 // k_solve's launch bound (2 CTAs per SM): the prefix-reusing TIME evaluator
-// runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120);
-// the other evaluators keep 16 warps at 64 registers (at 56 the CAPACITY
-// thread evaluator spills: -16 % on j120)
+// runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120;
+// 20 warps at 48: +1.4 % j120p, -1…-4 % on j30p/j60p, profiles/r2/
+// ab_launch_bounds.txt), so does the CAPACITY warp evaluator (+2.5…3.4 % on
+// j60p/j120p/j120 over 16 warps, -3 % j30p); the thread-per-schedule one keeps
+// 16 warps at 64 registers (at 56 it spills: -16 % on j120)
 #ifndef CAP_THREADS
-#define CAP_THREADS 512
+#define CAP_THREADS 576
+#endif
+#ifndef TIME_THREADS
+#define TIME_THREADS 576
 #endif
 constexpr int ksolve_threads(int mode, int G) {
-  return mode == MODE_TIME && G == 32 ? 576 : (mode == MODE_CAPACITY && G == 32 ? CAP_THREADS : 512);
+  return mode == MODE_TIME && G == 32 ? TIME_THREADS
+                                      : (mode == MODE_CAPACITY && G == 32 ? CAP_THREADS : 512);
 }
-constexpr int KSOLVE_THREADS_MAX = 576;
+constexpr int KSOLVE_THREADS_MAX = TIME_THREADS > CAP_THREADS ? (TIME_THREADS > 512 ? TIME_THREADS : 512)
+                                                              : (CAP_THREADS > 512 ? CAP_THREADS : 512);
 
 // =========================================================================
 // K1: batch evaluation
