@@ -65,8 +65,10 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
 
 // k_solve's launch bound (2 CTAs per SM): the prefix-reusing TIME evaluator
 // runs 18 warps per CTA at 56 registers (+4 % over 16 warps at 64 on j120;
-// 20 warps at 48: +1.4 % j120p, -1…-4 % on j30p/j60p, profiles/r2/
-// ab_launch_bounds.txt), so does the CAPACITY warp evaluator (+2.5…3.4 % on
+// 20 warps at 48: +1.2…1.6 % on j120p/j120 but -1…-4 % on j30p/j60p, so the
+// 20-warp instantiation, TIME_THREADS_LARGE, serves projects above 64
+// activities only; profiles/r2/ab_launch_bounds.txt), so does the CAPACITY
+// warp evaluator (+2.5…3.4 % on
 // j60p/j120p/j120 over 16 warps, -3 % j30p); the thread-per-schedule one keeps
 // 16 warps at 64 registers (at 56 it spills: -16 % on j120)
 #ifndef CAP_THREADS
@@ -74,6 +76,9 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
 #endif
 #ifndef TIME_THREADS
 #define TIME_THREADS 576
+#endif
+#ifndef TIME_THREADS_LARGE
+#define TIME_THREADS_LARGE 640
 #endif
 constexpr int ksolve_threads(int mode, int G) {
   return mode == MODE_TIME && G == 32 ? TIME_THREADS
@@ -981,9 +986,9 @@ __device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restri
   }
 }
 
-template <int MODE, int G, int W>
-__global__ void __launch_bounds__(ksolve_threads(MODE, G), 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
-                                                  int n_ids, SmemPlan plan) {
+template <int MODE, int G, int W, int LB = ksolve_threads(MODE, G)>
+__global__ void __launch_bounds__(LB, 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
+                                                 int n_ids, SmemPlan plan) {
   solve_body<MODE, G, W>(A, ids, n_ids, plan);
 }
 
@@ -1371,6 +1376,27 @@ int rcpsp_solve(const RcpspSolveArgs* args, const int32_t* inst_ids, int n_ids, 
                          static_cast<int>(A.sumcap_max)))
       return fail("search state does not fit in shared memory");
     auto k = k_solve<MODE, G, W>;
+#if TIME_THREADS_LARGE > 0
+    // TIME on projects above 64 activities: 20 warps per CTA at 48 registers
+    // when two such CTAs fit per SM (A/B on B200: +1.4 % on j120p; projects of
+    // <= 64 activities run smaller CTAs at 56 registers, where 48 cost 1-4 %,
+    // profiles/r2/ab_launch_bounds.txt)
+    if constexpr (MODE == MODE_TIME && G == 32) {
+      SmemPlan q;
+      int tq;
+      if (threads == 0 && A.n_max > 64 &&
+          fit_plan_limit(MODE, G, static_cast<int>(A.words), static_cast<int>(A.n_max),
+                         static_cast<int>(A.m_max), static_cast<int>(A.h_max),
+                         static_cast<int>(A.e_max), static_cast<int>(A.rmax_max),
+                         static_cast<int>(A.delta), static_cast<int>(A.tabu_size),
+                         TIME_THREADS_LARGE, smem_per_sm() / 2 - 1024, TIME_THREADS_LARGE, q, tq,
+                         A.no_big ? 0 : 1, static_cast<int>(A.sumcap_max))) {
+        p = q;
+        nt = tq;
+        k = k_solve<MODE, G, W, TIME_THREADS_LARGE>;
+      }
+    }
+#endif
     // Alternatives when the plan above is shared-memory-limited, the one that
     // keeps the most threads resident per SM wins (ties: the plan above):
     //  * the wide variant (one CTA per SM, up to 32 warps at 64 registers);
