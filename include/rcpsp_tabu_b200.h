@@ -257,7 +257,9 @@ int rcpsp_diversify_batch(const int32_t *blob, const RcpspShape *shape, int32_t 
  * (kernels.py:68-146 via evaluator.py:69-107): op 0 = cap_earliest_start,
  * 1 = cap_update (arg = start), 2 = time_earliest_start (arg = es_prec),
  * 3 = time_update (arg = start).  state: CAP int32 [m][R_max], TIME int32
- * [m][H+1] (updated in place); out[0] receives the earliest start. */
+ * [m][H+1] (updated in place); out[0] receives the earliest start.  A
+ * cap_update start below the activity's Eq. 7 bound (cap_earliest_start) is
+ * refused with error word 8 and the state left as it was. */
 int rcpsp_state_op(const int32_t *blob, const RcpspShape *shape, int op, int32_t *state, int act, int arg, int32_t *out,
                    int32_t *err, void *stream);
 

@@ -33,7 +33,8 @@ constexpr int TAU_PAD = 32;
 enum DevErr {
   DE_OK = 0, DE_BAD_BLOB = 1, DE_NO_WINDOW = 2, DE_SMEM = 3, DE_TABU_BAND = 4, DE_CYCLE = 5,
   DE_BAD_MOVE = 6,
-  DE_POOL_MIN = 7  // global best above a pool entry (cooperation.py:76-79 invariant)
+  DE_POOL_MIN = 7,  // global best above a pool entry (cooperation.py:76-79 invariant)
+  DE_CAP_START = 8  // rcpsp_state_op cap_update below the Eq. 7 bound (see k_state_op)
 };
 
 __device__ __forceinline__ void set_err(int* err, int code) {

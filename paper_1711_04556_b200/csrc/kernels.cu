@@ -324,6 +324,12 @@ __global__ void __launch_bounds__(32) k_state_op(const int* __restrict__ blob, R
     return;
   }
   if (op == OP_CAP_UPDATE) {  // the SGS's warp-wide closed form of Alg. 4
+    // the closed form holds for starts at or above Eq. 7's bound -- the only
+    // ones an SGS produces; a start below it is refused, state untouched
+    if (dur > 0 && arg < cap_es(state, 1, dem, I.cap, m, R)) {
+      if (lane == 0) set_err(err, DE_CAP_START);
+      return;
+    }
     int* st = smem + used;
     for (int j = lane; j < m * R; j += 32) st[j] = state[j];
     __syncwarp();

@@ -370,7 +370,12 @@ def state_op(inst: ProjectInstance, op: str, state: np.ndarray, act: int, arg: i
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     check(L.rcpsp_state_op(ptr(di.blob), ctypes.byref(di.shape), STATE_OPS[op], ptr(d_state), int(act), int(arg),
                            ptr(out), ptr(err), stream_handle()), "rcpsp_state_op")
-    if int(err.cpu()[0]):
+    code = int(err.cpu()[0])
+    if code == 8:
+        raise ValueError(f"cap_update start {arg} below the capacity bound (Eq. 7) of "
+                         f"activity {act}: the closed-form update needs a start an SGS "
+                         "could produce")
+    if code:
         raise ValueError("resource state holds values outside the packed lane range")
     if op.endswith("update"):
         state[...] = d_state.cpu().numpy().reshape(state.shape)
@@ -400,7 +405,8 @@ def smem_bandwidth(iters: int = 4096, reps: int = 5) -> float:
 DEV_ERRORS = {1: "bad instance blob", 2: "no resource window before the horizon "
               "(demand above capacity?)", 3: "shared memory plan", 4: "tabu move outside the "
               "delta band", 5: "precedence cycle", 6: "bad move",
-              7: "pool-min invariant violated: global best above a pool entry"}
+              7: "pool-min invariant violated: global best above a pool entry",
+              8: "cap_update start below the capacity bound (Eq. 7)"}
 
 
 def _raise_dev_err(err) -> None:

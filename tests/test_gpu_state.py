@@ -11,7 +11,7 @@ from conftest import random_topological_order
 
 pytestmark = pytest.mark.gpu
 
-from paper_1711_04556_b200 import make_instance, synth  # noqa: E402
+from paper_1711_04556_b200 import device, make_instance, synth  # noqa: E402
 from paper_1711_04556_b200.evaluator import (CapacityResourceState,  # noqa: E402
                                              TimeResourceState, cap_earliest_start, cap_update,
                                              time_earliest_start, time_update)
@@ -129,3 +129,23 @@ def test_cap_update_closed_form_random_rows():
         oracle.cap_update(inst, ref, 1, s)
         assert (st.levels == ref).all(), (trial, caps, dem, dur, s)
         assert st.rows_descending()
+
+
+def test_cap_update_below_bound_refused():
+    """A cap_update start below Eq. 7's bound (no SGS produces one) is refused
+    loudly with the state untouched, instead of a silently different row."""
+    inst = one_resource(4, [0, 3, 2, 0], [0, 3, 2, 0], [[1, 2], [3], [3], []])
+    st = CapacityResourceState(inst)
+    cap_update(st, 1, 0, inst)
+    es = cap_earliest_start(st, 2, inst)
+    assert es == 3
+    before = st.levels.copy()
+    with pytest.raises(ValueError, match="below the earliest resource start"):
+        cap_update(st, 2, es - 1, inst)          # the host mirror refuses first
+    with pytest.raises(ValueError, match="below the capacity bound"):
+        device.state_op(inst, "cap_update", st.levels, 2, es - 1)  # the C ABI itself
+    assert (st.levels == before).all()
+    cap_update(st, 2, es, inst)
+    ref = before.copy()
+    oracle.cap_update(inst, ref, 2, es)
+    assert (st.levels == ref).all()
