@@ -35,6 +35,20 @@ extern "C" {
 
 #define RCPSP_ABI_VERSION 8
 
+/* Values of the device error word (the `err` argument / RcpspSolveArgs.err):
+ * the first error a kernel hits is kept. */
+enum {
+    RCPSP_DE_OK = 0,
+    RCPSP_DE_BAD_BLOB = 1,    /* blob header does not match RcpspShape           */
+    RCPSP_DE_NO_WINDOW = 2,   /* no resource window before the horizon           */
+    RCPSP_DE_SMEM = 3,        /* shared-memory plan broken (e.g. no_big violated) */
+    RCPSP_DE_TABU_BAND = 4,   /* tabu move outside the delta band                */
+    RCPSP_DE_CYCLE = 5,       /* precedence cycle                                */
+    RCPSP_DE_BAD_MOVE = 6,    /* malformed move                                  */
+    RCPSP_DE_POOL_MIN = 7,    /* global best above a pool entry (cooperation.py:76-79) */
+    RCPSP_DE_CAP_START = 8    /* rcpsp_state_op cap_update below the Eq. 7 bound */
+};
+
 /* Everything the on-device orchestrate needs (all fields 64-bit so the ctypes
  * mirror in device.py is a flat array).  Sizes: I = instances in the batch,
  * B = workers (CTAs) per instance, F = pool_size, T = tabu_size,

@@ -21,6 +21,11 @@
 #include "sgs.cuh"
 
 using namespace rt;
+static_assert(rt::DE_BAD_BLOB == RCPSP_DE_BAD_BLOB && rt::DE_NO_WINDOW == RCPSP_DE_NO_WINDOW &&
+                  rt::DE_SMEM == RCPSP_DE_SMEM && rt::DE_TABU_BAND == RCPSP_DE_TABU_BAND &&
+                  rt::DE_CYCLE == RCPSP_DE_CYCLE && rt::DE_BAD_MOVE == RCPSP_DE_BAD_MOVE &&
+                  rt::DE_POOL_MIN == RCPSP_DE_POOL_MIN && rt::DE_CAP_START == RCPSP_DE_CAP_START,
+              "device error codes: common.cuh and the public header agree");
 
 namespace {
 
