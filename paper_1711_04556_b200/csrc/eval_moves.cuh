@@ -73,7 +73,11 @@ __device__ __noinline__ void eval_moves_time32(int o_info, int o_pull, int o_req
 //   the prefix, and the move is evaluated exactly by the full-horizon SGS on
 //   the CTA's fallback region o_fb (one warp at a time, lock at o_fblock);
 //   o_info_f / o_push: the push records and successor lists it needs.
-template <int W, bool BIG, bool SIZED>
+//   LONG: phase B tests its loop once per eight positions instead of four --
+//   used by the large-project search kernel only (k_solve at
+//   TIME_THREADS_LARGE; A/B on B200: +1.6 % j120p, +1.4 % Gen-R j120; in
+//   every kernel it cost j60p 1.8 %, profiles/r2/ab_phaseb8.txt)
+template <int W, bool BIG, bool SIZED, bool LONG = false>
 __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o_req, int o_base,
                                                    int o_bst, int o_ctr, int o_evs, uint32_t cap0,
                                                    uint32_t cap1, uint32_t hi, int n, int H,
@@ -246,9 +250,22 @@ __device__ __noinline__ void eval_moves_time32_inc(int o_info, int o_pull, int o
       };
       // one loop test per four positions (branches cost more than their
       // instructions here), then a pair and a single step for the rest
-      while (p + 3 < pend && !(SIZED && ovf)) {
-        pair();
-        pair();
+      if constexpr (LONG) {  // one test per eight positions on long suffixes
+        while (p + 7 < pend && !(SIZED && ovf)) {
+          pair();
+          pair();
+          pair();
+          pair();
+        }
+        if (p + 3 < pend && !(SIZED && ovf)) {
+          pair();
+          pair();
+        }
+      } else {
+        while (p + 3 < pend && !(SIZED && ovf)) {
+          pair();
+          pair();
+        }
       }
       if (p + 1 < pend && !(SIZED && ovf)) pair();
       if (p < pend && !(SIZED && ovf)) {
@@ -626,7 +643,7 @@ __device__ __forceinline__ uint32_t cluster_counter(const CtaCtx& c) {
 }
 
 // the prefix-reusing TIME evaluator on this CTA's copy of the current order
-template <int W>
+template <int W, bool LONG = false>
 // (noinline: keeps the evaluators' argument set out of the search loop's
 // register allocation -- A/B on B200, profiles/r2/ab_dispatch_noinline.txt:
 // j30 +10 %, j30p +6 %, j60p +2 %, j120p +0.5 %, j120p CAPACITY +1.3 %)
@@ -645,6 +662,12 @@ __device__ __noinline__ void eval_moves_time32_dispatch(const CtaCtx& c, int n_f
         soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
         c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax, c.err, ctr_cl,
         c.slots, soff(c.fb), soff(c.scal + SC_FBLOCK), soff(c.I.info_f), soff(c.I.sdat));
+  else if (LONG)
+    eval_moves_time32_inc<W, false, false, true>(
+        soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req), soff(c.base), soff(c.bst),
+        soff(c.scal + SC_CTR), soff(c.evs), c.I.capw[0], W == 2 ? c.I.capw[1] : 0u, c.I.hi,
+        c.I.n, c.I.H, c.moves_buf, c.cmax_buf, n_feas, c.warp_words, base_cmax, c.err, ctr_cl,
+        full, 0, 0, 0, 0);
   else
     eval_moves_time32_inc<W, false, false>(
         soff(c.I.info_r), soff(c.I.pdat), soff(c.I.req), soff(c.base), soff(c.bst),
@@ -676,7 +699,7 @@ __device__ __noinline__ void eval_moves_cap_warp_dispatch(const CtaCtx& c, int n
 // phase), copy the current order and its starts from the leader's shared
 // memory, deal moves from the leader's counter, write makespans into the
 // leader's global buffer, B2.  The instance follows the leader's (steals).
-template <int MODE, int G, int W>
+template <int MODE, int G, int W, bool LONG = false>
 //   blob/blob_off: the launch's instances (blob_off null: one instance)
 __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, int iid, int* smem,
                            int plan_inst, int csize) {
@@ -708,7 +731,7 @@ __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, 
     __syncthreads();
     const uint32_t ctr = l_scal + 4 * SC_CTR;
     if constexpr (MODE == MODE_TIME) {
-      eval_moves_time32_dispatch<W>(c, n_feas, base_cmax, ctr);
+      eval_moves_time32_dispatch<W, LONG>(c, n_feas, base_cmax, ctr);
     } else if constexpr (G == 32) {
       eval_moves_cap_warp_dispatch(c, n_feas, true, ctr, base_cmax);
     } else {
@@ -724,7 +747,7 @@ __device__ void cta_follow(CtaCtx& c, const int* blob, const int64_t* blob_off, 
 }
 
 // every compacted move -> cmax_buf (full SGS of the swapped order)
-template <int MODE, int G, int W>
+template <int MODE, int G, int W, bool LONG = false>
 __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
   if constexpr (MODE == MODE_TIME) {
     if constexpr (G == 32) {
@@ -751,7 +774,7 @@ __device__ __forceinline__ void cta_eval_moves(CtaCtx& c, int n_feas) {
         }
         __syncthreads();
         cluster_phase_begin(c, n_feas);
-        eval_moves_time32_dispatch<W>(c, n_feas, c.scal[SC_BASEC], cluster_counter(c));
+        eval_moves_time32_dispatch<W, LONG>(c, n_feas, c.scal[SC_BASEC], cluster_counter(c));
         cluster_phase_end(c);
       } else {
         eval_moves_time32<W>(soff(c.I.info_f), soff(c.I.sdat), soff(c.I.req), soff(c.base),

@@ -85,7 +85,7 @@ __device__ __forceinline__ bool shape_ok(const int* __restrict__ blob, const Rcp
 #ifndef TIME_THREADS_LARGE
 #define TIME_THREADS_LARGE 640
 #endif
-constexpr int ksolve_threads(int mode, int G) {
+__host__ __device__ constexpr int ksolve_threads(int mode, int G) {
   return mode == MODE_TIME && G == 32 ? TIME_THREADS
                                       : (mode == MODE_CAPACITY && G == 32 ? CAP_THREADS : 512);
 }
@@ -736,7 +736,7 @@ __device__ void import_peer_elite(const RcpspSolveArgs& A, CtaCtx& c, int iid, i
 // path) moves on to the next instance of the launch that still has budget,
 // so the batch finishes together; without it (the reference's fixed
 // worker-to-pool mapping, and exact B = 1 trajectories) it exits.
-template <int MODE, int G, int W>
+template <int MODE, int G, int W, bool LONG = false>
 __device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restrict__ ids, int n_ids,
                                            const SmemPlan& plan) {
   int* smem = dsm;
@@ -771,7 +771,7 @@ __device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restri
   if constexpr ((MODE == MODE_TIME && G == 32) || MODE == MODE_CAPACITY) {
     if (C > 1) {
       if (cluster_rank() != 0) {
-        cta_follow<MODE, G, W>(c, A.blob, A.blob_off, iid, smem, plan.inst, C);
+        cta_follow<MODE, G, W, LONG>(c, A.blob, A.blob_off, iid, smem, plan.inst, C);
         return;
       }
       c.csize = C;
@@ -957,7 +957,7 @@ __device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restri
     const int start_cmax = cta_eval_one<MODE, G, W>(c, c.base);
     for (int p = tid; p < c.I.n; p += blockDim.x) c.best[p] = c.base[p];
     __syncthreads();
-    ChunkOut o = run_chunk_cta<MODE, G, W>(c, static_cast<int>(granted), adopted, start_cmax,
+    ChunkOut o = run_chunk_cta<MODE, G, W, LONG>(c, static_cast<int>(granted), adopted, start_cmax,
                                            best_known, c.I.cpm,
                                            wtrace ? wtrace + tlen : nullptr);
     used = o.iters;
@@ -1000,7 +1000,8 @@ __device__ __forceinline__ void solve_body(RcpspSolveArgs A, const int* __restri
 template <int MODE, int G, int W, int LB = ksolve_threads(MODE, G)>
 __global__ void __launch_bounds__(LB, 2) k_solve(RcpspSolveArgs A, const int* __restrict__ ids,
                                                  int n_ids, SmemPlan plan) {
-  solve_body<MODE, G, W>(A, ids, n_ids, plan);
+  // the large-project instantiation also takes the long-suffix evaluator
+  solve_body<MODE, G, W, (LB != ksolve_threads(MODE, G))>(A, ids, n_ids, plan);
 }
 
 // One CTA per SM with up to 32 warps (64 registers), for launches whose

@@ -29,7 +29,7 @@ struct ChunkOut {
 
 // kernels.py:316-385.  c.base holds the order (mutated in place), the tabu
 // list/counters/head are in shared memory.  trace may be null.
-template <int MODE, int G, int W>
+template <int MODE, int G, int W, bool LONG = false>
 __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int start_cmax,
                                   int best_known_cmax, int floor_cmax, int* trace) {
   const int tid = threadIdx.x, n = c.I.n;
@@ -43,7 +43,7 @@ __device__ ChunkOut run_chunk_cta(CtaCtx& c, int budget, int adopted_cmax, int s
       if (tid == 0 && trace) trace[iters - 1] = cur;
       break;
     }
-    cta_eval_moves<MODE, G, W>(c, n_feas);
+    cta_eval_moves<MODE, G, W, LONG>(c, n_feas);
     evals += n_feas;
     const bool counted =
         MODE == MODE_CAPACITY ? (G == 32 || (c.inc && n >= 48)) : (G == 32 && c.inc);
