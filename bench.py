@@ -338,8 +338,9 @@ PER_CONFIG = (("j60p", "time", 8, 1000), ("j60p", "capacity", 8, 1000),
 def per_config_entry(args, cfg: str, mode: str, workers: int, iters: int, smem_peak: float,
                      cpu_count: int) -> dict:
     """One compact measurement of another BASELINE config: the synth batch of
-    DEFAULT_BATCH instances, mode forced, 1 warm-up + 2 timed steps (CUDA
-    events around pool init + search, L2 flushed), its roofline fraction with
+    DEFAULT_BATCH instances, mode forced, warm-up steps for >= 0.5 s of device
+    time, then 1 more + 2 timed steps (CUDA events around pool init + search,
+    L2 flushed), its roofline fraction with
     the same SMEM peak, and its own cpu_baseline on the config's CPU sample
     (as many sample instances as fit ~4 s on all host cores, >= 2)."""
     import torch
@@ -356,6 +357,21 @@ def per_config_entry(args, cfg: str, mode: str, workers: int, iters: int, smem_p
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
     ms, sms, evals, sevals, steps, devs = 0.0, 0.0, 0, 0, 0, []
+    # warm-up until >= 0.5 s of device time (at least one step): short steps
+    # otherwise meet the clocks still ramping after the CPU legs left the GPU
+    # idle (one j60p step is ~44 ms)
+    warm_ms, k = 0.0, 0
+    while k == 0 or warm_ms < 500.0:
+        solver.reset()
+        torch.cuda.synchronize()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        solver.pool_init(stream)
+        solver.search(stream=stream)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        warm_ms += w0.elapsed_time(w1)
+        k += 1
     for k in range(3):
         solver.reset()
         flush.fill_(1)
