@@ -95,6 +95,22 @@ def _rest(sections, rng, j30, j60, big) -> None:
                     assert int(r.evaluations[i]) == want["evaluations"], (i, mode, cluster)
             else:
                 assert ((r.iterations == 30) | (r.best_cmax == r.critical_path)).all()
+    # the large-project search kernel (TIME, > 64 activities: 20-warp CTAs,
+    # long-suffix loop) and CAPACITY on the same instances
+    big_insts = synth.benchmark_batch("j120p", 2, first_seed=3)
+    for mode in ((1, 0) if "K3L" in sections else ()):
+        for workers in (1, 2):
+            cfg = SolveConfig(total_iters=12, workers=workers, pool_size=4, tabu_size=60,
+                              delta=30, phi_steps=5, phi_max=1, seed=1, cluster=1)
+            r = BatchSolver(big_insts, [mode] * 2, cfg).run()
+            if workers == 1:
+                for i, inst in enumerate(big_insts):
+                    want = oracle.orchestrate(inst, 12, 1, 1, mode, delta=30, tabu_size=60,
+                                              phi_steps=5, phi_max=1, pool_size=4)
+                    assert int(r.best_cmax[i]) == want["best_cmax"], ("K3L", mode, i)
+                    assert int(r.evaluations[i]) == want["evaluations"], ("K3L", mode, i)
+    if "K3L" in sections:
+        print("K3L ok", flush=True)
     # TIME with makespan-bounded per-warp profiles forced tight (fallback path)
     j60 = synth.benchmark_batch("j60p", 2, first_seed=0)
     for slots in (160, 96) if "sized" in sections else ():
@@ -122,7 +138,7 @@ def _rest(sections, rng, j30, j60, big) -> None:
     print("K0/K3/K4 ok", flush=True)
 
 
-ALL = {"K1", "misc", "K2", "K3", "sized", "K4"}
+ALL = {"K1", "misc", "K2", "K3", "K3L", "sized", "K4"}
 
 if __name__ == "__main__":
     main(set(sys.argv[1:]) or ALL)
