@@ -700,3 +700,23 @@ def test_decide_dynamic_on_the_device():
     # (orchestrate re-evaluates the stored best order and checks it feasible)
     assert ctl.measurements >= 2 and st.feasible
     assert st.iterations <= 300 and st.best_cmax >= st.critical_path
+
+
+def test_large_project_kernel_shapes_vs_oracle():
+    """The large-project search kernel (projects above 64 activities: 20-warp
+    CTAs, long-suffix phase-B loop) on both TIME packings (one and two words
+    per slot) and on CAPACITY: B = 1 trajectories equal to the oracle's."""
+    from paper_1711_04556_b200.device import BatchSolver, SolveConfig
+    insts = [synth.random_instance(90, 3, seed=71, cap_lo=6, cap_hi=20),           # W = 1
+             synth.random_instance(80, 6, seed=72, cap_lo=6, cap_hi=20),           # W = 2
+             synth.benchmark_batch("j120p", 1, first_seed=77)[0]]
+    for mode in (1, 0):
+        cfg = SolveConfig(total_iters=40, workers=1, pool_size=6, tabu_size=60, delta=30,
+                          phi_steps=20, phi_max=3, seed=9, collect_trace=True)
+        for inst in insts:  # one launch per packing (TIME groups by words)
+            r = BatchSolver([inst], [mode], cfg).run()
+            want = oracle.orchestrate(inst, 40, 1, 9, mode, delta=30, tabu_size=60, pool_size=6,
+                                      collect_trace=True)
+            assert int(r.best_cmax[0]) == want["best_cmax"], (inst.name, mode)
+            assert int(r.evaluations[0]) == want["evaluations"], (inst.name, mode)
+            assert [t.tolist() for t in r.traces[0]] == [t.tolist() for t in want["traces"]]
